@@ -42,7 +42,7 @@ import numpy as np
 
 __all__ = [
     "grunwald_g", "wsgd_w", "toeplitz_T", "symbol_g", "symbol_w", "symbol_p",
-    "symbol_q", "symbol_F", "theta_grid", "sine_matrix", "tau_matrix",
+    "symbol_q", "symbol_F", "theta_grid", "sine_matrix", "sine_mode", "tau_matrix",
     "System", "pcg", "gmres", "lu_solve", "cond2",
     "PREC_NONE", "PREC_TAU", "PREC_TAU_D", "PREC_TAU_DSYM", "PREC_TILDE",
     "example1_matrices", "example1_run", "example2_matrices", "example2_run",
@@ -145,6 +145,18 @@ def sine_matrix(n: int) -> np.ndarray:
     return math.sqrt(2.0 / m) * np.sin(math.pi * ij.astype(np.float64) / m)
 
 
+def sine_mode(n: int, i: int, j: int = None) -> np.ndarray:
+    """Column i (1-based) of S_n (1D) or the Kronecker mode (S⊗S)e_{(i,j)}
+    (2D, x index i, y index j) as an x-fastest vector: an eigenvector of every
+    τ matrix, so τ(F)⁻¹ mode = mode / F(i, j)."""
+    m = n + 1
+    k = np.arange(1, n + 1, dtype=np.int64)
+    col = lambda c: math.sqrt(2.0 / m) * np.sin(math.pi * np.mod(k * c, 2 * m).astype(np.float64) / m)
+    if j is None:
+        return col(i)
+    return np.outer(col(j), col(i)).reshape(-1)
+
+
 def tau_matrix(samples: np.ndarray) -> np.ndarray:
     """τ_n(f) = S_n·diag(f(θ_{j,n}))·S_n (P:L31, eq:tau)."""
     S = sine_matrix(len(samples))
@@ -203,6 +215,26 @@ class System:
              + self.ywt * (self.ep.reshape(n, n) * (self.Tb @ X)      # (T_β⊗I)x: T_β on each y-line
                            + self.em.reshape(n, n) * (self.Tb.T @ X)))  # (T_βᵀ⊗I)x
         return Y.reshape(-1)
+
+    def matvec_entries(self, x: np.ndarray, idx) -> np.ndarray:
+        """Selected entries (flat x-fastest indices) of M x, each written out
+        from the definition one by one (for sizes where the full dense
+        product is too slow)."""
+        x = np.asarray(x, dtype=np.float64)
+        out = np.empty(len(idx))
+        n = self.n
+        if self.dims == 1:
+            for t, i in enumerate(idx):
+                out[t] = (self.nu * x[i] + self.dp[i] * (self.Ta[i, :] @ x)
+                          + self.dm[i] * (self.Ta[:, i] @ x))
+            return out
+        X = x.reshape(n, n)
+        for t, e in enumerate(idx):
+            j, i = divmod(int(e), n)
+            out[t] = (self.nu * X[j, i]
+                      + self.dp[e] * (self.Ta[i, :] @ X[j, :]) + self.dm[e] * (self.Ta[:, i] @ X[j, :])
+                      + self.ywt * (self.ep[e] * (self.Tb[j, :] @ X[:, i]) + self.em[e] * (self.Tb[:, j] @ X[:, i])))
+        return out
 
     def dense(self) -> np.ndarray:
         """The N×N matrix, assembled with Kronecker products (small n only)."""

@@ -1,0 +1,975 @@
+// Host driver + C ABI (include/fde.h) of the B200 hot path.
+//
+// Setup: Grünwald weights g_k or weighted-shifted
+// weights w_k (γ = α), the circulant embedding of T_α
+// and its eigenvalues λ = DFT_L(c), the symbol samples
+// F_α(θ_j) (P:L245 / P:L253, closed forms) and the diagonal D (P:L279,
+// P:L384). Everything per-iteration runs in the kernels of
+// line_kernels.cuh / krylov_kernels.cuh; the host only enqueues work
+// (captured once into CUDA graphs for the Krylov loops).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/fde.h"
+#include "krylov_kernels.cuh"
+#include "line_kernels.cuh"
+
+using namespace fde;
+
+namespace {
+
+struct FdeFail {
+  fde_status s;
+  std::string msg;
+};
+
+#define FDE_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw FdeFail{e_ == cudaErrorMemoryAllocation ? FDE_ERR_OUT_OF_MEMORY : FDE_ERR_CUDA, \
+                    std::string(#call) + ": " + cudaGetErrorString(e_)};                \
+  } while (0)
+
+constexpr int KMIN = 6, KMAX = 13, KR = 4;
+
+// ------------------------------------------------------------------ host maths
+std::vector<double> grunwald(double alpha, int K) {  // g_k = (-1)^k C(α,k)
+  std::vector<double> g(K + 1);
+  g[0] = 1.0;
+  for (int k = 1; k <= K; ++k) g[k] = g[k - 1] * (1.0 - (alpha + 1.0) / k);
+  return g;
+}
+std::vector<double> stencil_coeffs(double alpha, int K, int stencil) {
+  std::vector<double> g = grunwald(alpha, K);
+  if (stencil == 1) return g;
+  std::vector<double> w(K + 1);  // P:L162-163 with γ = α
+  w[0] = 0.5 * alpha * g[0];
+  for (int k = 1; k <= K; ++k) w[k] = 0.5 * alpha * g[k] + 0.5 * (2.0 - alpha) * g[k - 1];
+  return w;
+}
+
+// exp(-2πi e/L) with the angle reduced to the first octant for accuracy
+std::complex<double> root_of_unity(long long e, long long L) {
+  e %= L;
+  if (e < 0) e += L;
+  // angle = 2π e / L ; use symmetry: quadrant
+  const long long q4 = L / 4;
+  if (L % 4 == 0) {
+    const long long quad = e / q4, r = e % q4;
+    const double th = 2.0 * M_PI * (double)r / (double)L;
+    double c, s;
+    if (2 * r <= q4) { c = std::cos(th); s = std::sin(th); }
+    else { const double t2 = 2.0 * M_PI * (double)(q4 - r) / (double)L; c = std::sin(t2); s = std::cos(t2); }
+    // (c + i s) = exp(i th) rotated by quad quarter turns
+    std::complex<double> z(c, s);
+    for (long long i = 0; i < quad; ++i) z = std::complex<double>(-z.imag(), z.real());
+    return std::conj(z);
+  }
+  const double th = 2.0 * M_PI * (double)e / (double)L;
+  return std::complex<double>(std::cos(th), -std::sin(th));
+}
+
+// in-place iterative radix-2 DFT, X_k = Σ x_j exp(-2πi jk/L)
+void host_fft(std::vector<std::complex<double>>& a) {
+  const int L = (int)a.size();
+  for (int i = 1, j = 0; i < L; ++i) {
+    int bit = L >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (int len = 2; len <= L; len <<= 1) {
+    for (int i = 0; i < L; i += len)
+      for (int j = 0; j < len / 2; ++j) {
+        const std::complex<double> w = root_of_unity((long long)j * (L / len), L);
+        const std::complex<double> u = a[i + j], v = a[i + j + len / 2] * w;
+        a[i + j] = u + v;
+        a[i + j + len / 2] = u - v;
+      }
+  }
+}
+
+// symbols in closed form: s = 2 sin(θ/2), φ = (θ-π)/2
+double symbol_p(double a, double th) {  // p_α = g_α(θ) + g_α(-θ)
+  const double s = 2.0 * std::sin(0.5 * th), phi = 0.5 * (th - M_PI);
+  return -2.0 * std::pow(s, a) * std::cos(a * phi - th);
+}
+double symbol_q(double a, double th) {  // q_α = w_α(θ) + w_α(-θ)
+  const double s = 2.0 * std::sin(0.5 * th), phi = 0.5 * (th - M_PI);
+  return -2.0 * std::pow(s, a) * std::cos(a * phi) + a * std::pow(s, a + 1.0) * std::cos((a - 1.0) * phi);
+}
+
+int ilog2_exact(long long v) {
+  int k = 0;
+  while ((1LL << k) < v) ++k;
+  return (1LL << k) == v ? k : -1;
+}
+
+int bitrev_host(int x, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) { r = (r << 1) | (x & 1); x >>= 1; }
+  return r;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// ------------------------------------------------------- launch geometry
+template <int K, bool COL, int NBUF>
+struct LaunchCfg {
+  using G = FftGeom<K, KR>;
+  static constexpr int SPG = G::SM_STRIDE * 16 * NBUF;      // smem bytes per FFT group
+  static constexpr int SMEM_CAP = 200 * 1024;
+  static constexpr int MAXT = NBUF == 2 ? 256 : 512;        // threads per CTA (register budget)
+  static constexpr int BY_SMEM = SMEM_CAP / SPG > 0 ? SMEM_CAP / SPG : 1;
+  static constexpr int BY_THR = MAXT / G::P > 0 ? MAXT / G::P : 1;
+  static constexpr int WANT = COL ? 8 : (256 / G::P > 0 ? 256 / G::P : 1);
+  static constexpr int FPC = WANT < BY_SMEM ? (WANT < BY_THR ? WANT : BY_THR) : (BY_SMEM < BY_THR ? BY_SMEM : BY_THR);
+  static constexpr int THREADS = FPC * G::P;
+  static constexpr int SMEM = FPC * SPG;
+  static constexpr bool FITS = SPG <= 227 * 1024;
+};
+
+}  // namespace
+
+// ======================================================================== handle
+struct fde_handle_s {
+  fde_desc d{};
+  cudaStream_t st = nullptr;
+  int n = 0, m = 0, L = 0, K = 0, N = 0, batch = 1, dims = 1;
+  bool var_x = false, var_y = false;
+  std::string err;
+  long long launches = 0;
+
+  // tables
+  double2* tw = nullptr;
+  double2 *mu_x = nullptr, *mu_y = nullptr;
+  double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
+  double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
+  double *invF = nullptr, *Fx = nullptr, *Fy = nullptr;
+  double fscale = 0.0;
+  double *dpre = nullptr, *dpost = nullptr;
+  double cx = 1.0, cy = 1.0;
+  // workspace
+  double *wx = nullptr, *t1 = nullptr, *t2 = nullptr, *t3 = nullptr;
+  double *hin = nullptr, *hout = nullptr;  // staging for host pointers
+  // Krylov
+  SolveState* sst = nullptr;
+  GmresSmall* gsm = nullptr;
+  Counters* ctr = nullptr;
+  double* part = nullptr;
+  double *kx = nullptr, *kb = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kq = nullptr;
+  double* V = nullptr;
+  int V_cols = 0;
+  // graphs
+  cudaGraphExec_t g_pcg = nullptr;
+  int g_pcg_chunk = 0, g_pcg_nodes = 0;
+  cudaGraphExec_t g_gm = nullptr;
+  int g_gm_restart = 0, g_gm_left = -1, g_gm_nodes = 0;
+  double g_rtol = -1.0;
+  int g_maxit = -1;
+
+  std::vector<void*> allocs;
+
+  template <class T>
+  T* dalloc(size_t count) {
+    void* p = nullptr;
+    FDE_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    allocs.push_back(p);
+    return (T*)p;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    T* p = dalloc<T>(v.size());
+    FDE_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return p;
+  }
+  size_t vec_elems() const { return (size_t)batch * N; }
+};
+
+namespace {
+
+LineArgs base_args(fde_handle h) {
+  LineArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = h->n;
+  a.N = h->N;
+  a.tw = h->tw;
+  return a;
+}
+
+// ------------------------------------------------------ kernel dispatchers
+template <int K, bool COL, bool VAR>
+void launch_toep_k(fde_handle h, const LineArgs& a) {
+  using C = LaunchCfg<K, COL, VAR ? 2 : 1>;
+  auto kern = k_toeplitz_lines<K, KR, COL, VAR, C::FPC>;
+  const int npairs = (a.nlines + 1) / 2;
+  const int grid = (npairs + C::FPC - 1) / C::FPC;
+  kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a);
+  FDE_CUDA(cudaGetLastError());
+  h->launches++;
+}
+template <int K, bool COL>
+void launch_dst_k(fde_handle h, const LineArgs& a) {
+  using C = LaunchCfg<K, COL, 1>;
+  auto kern = k_dst_lines<K, KR, COL, C::FPC>;
+  const int npairs = (a.nlines + 1) / 2;
+  kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a);
+  FDE_CUDA(cudaGetLastError());
+  h->launches++;
+}
+template <int K, bool COL>
+void launch_tau_k(fde_handle h, const LineArgs& a) {
+  using C = LaunchCfg<K, COL, 1>;
+  auto kern = k_tau_lines<K, KR, COL, C::FPC>;
+  const int npairs = (a.nlines + 1) / 2;
+  kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a);
+  FDE_CUDA(cudaGetLastError());
+  h->launches++;
+}
+
+#define FDE_SWITCH_K(K, CALL)                                           \
+  switch (K) {                                                          \
+    case 6: { constexpr int KK = 6; CALL; } break;                      \
+    case 7: { constexpr int KK = 7; CALL; } break;                      \
+    case 8: { constexpr int KK = 8; CALL; } break;                      \
+    case 9: { constexpr int KK = 9; CALL; } break;                      \
+    case 10: { constexpr int KK = 10; CALL; } break;                    \
+    case 11: { constexpr int KK = 11; CALL; } break;                    \
+    case 12: { constexpr int KK = 12; CALL; } break;                    \
+    case 13: { constexpr int KK = 13; CALL; } break;                    \
+    default: throw FdeFail{FDE_ERR_UNSUPPORTED, "transform length out of range"}; \
+  }
+
+template <int K>
+constexpr bool var_fused_fits() { return LaunchCfg<K, false, 2>::FITS; }
+
+template <int K, bool COL, bool VAR>
+void set_attr_toep() {
+  using C = LaunchCfg<K, COL, VAR ? 2 : 1>;
+  if (C::SMEM > 227 * 1024) return;
+  FDE_CUDA(cudaFuncSetAttribute(k_toeplitz_lines<K, KR, COL, VAR, C::FPC>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+}
+template <int K>
+void init_kernel_attrs() {
+  set_attr_toep<K, false, false>();
+  set_attr_toep<K, true, false>();
+  set_attr_toep<K, false, true>();
+  set_attr_toep<K, true, true>();
+  using C0 = LaunchCfg<K, false, 1>;
+  using C1 = LaunchCfg<K, true, 1>;
+  FDE_CUDA(cudaFuncSetAttribute(k_dst_lines<K, KR, false, C0::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C0::SMEM));
+  FDE_CUDA(cudaFuncSetAttribute(k_tau_lines<K, KR, false, C0::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C0::SMEM));
+  FDE_CUDA(cudaFuncSetAttribute(k_tau_lines<K, KR, true, C1::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM));
+}
+
+// One Toeplitz pass along rows (COL=false) or columns (COL=true).
+void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const double* yin, double nu, const int* gate) {
+  LineArgs a = base_args(h);
+  a.x = x;
+  a.y = y;
+  a.yin = yin;
+  a.nu = nu;
+  a.gate = gate;
+  a.nlines = h->dims == 1 ? h->batch : h->batch * h->n;
+  const bool var = col ? h->var_y : h->var_x;
+  if (!var) {
+    a.mu = col ? h->mu_y : h->mu_x;
+    if (col) { FDE_SWITCH_K(h->K, (launch_toep_k<KK, true, false>(h, a))); }
+    else { FDE_SWITCH_K(h->K, (launch_toep_k<KK, false, false>(h, a))); }
+    return;
+  }
+  a.lamS = col ? h->lamS_y : h->lamS_x;
+  a.lamK = col ? h->lamK_y : h->lamK_x;
+  a.cP = col ? h->cP_y : h->cP_x;
+  a.cM = col ? h->cM_y : h->cM_x;
+  bool fused = false;
+  FDE_SWITCH_K(h->K, (fused = var_fused_fits<KK>()));
+  if (fused) {
+    if (col) { FDE_SWITCH_K(h->K, (launch_toep_k<KK, true, true>(h, a))); }
+    else { FDE_SWITCH_K(h->K, (launch_toep_k<KK, false, true>(h, a))); }
+    return;
+  }
+  // too large for two buffers: symmetric and skew parts as two single-chain passes
+  double2* muS = reinterpret_cast<double2*>(col ? h->mu_y : h->mu_x);  // (Re λ, 0) / L
+  double2* muK = muS + h->L;                                             // (0, Im λ) / L
+  LineArgs a1 = a;
+  a1.mu = muS;
+  a1.omul = a.cP;
+  a1.y = y;
+  LineArgs a2 = a;
+  a2.mu = muK;
+  a2.omul = a.cM;
+  a2.nu = 0.0;
+  a2.yin = y;
+  a2.y = y;
+  if (col) {
+    FDE_SWITCH_K(h->K, (launch_toep_k<KK, true, false>(h, a1)));
+    FDE_SWITCH_K(h->K, (launch_toep_k<KK, true, false>(h, a2)));
+  } else {
+    FDE_SWITCH_K(h->K, (launch_toep_k<KK, false, false>(h, a1)));
+    FDE_SWITCH_K(h->K, (launch_toep_k<KK, false, false>(h, a2)));
+  }
+}
+
+// y = A x (a1)
+void op_matvec(fde_handle h, const double* x, double* y, const int* gate) {
+  if (h->dims == 1) {
+    toeplitz_pass(h, false, x, y, nullptr, h->d.nu, gate);
+  } else {
+    toeplitz_pass(h, false, x, h->wx, nullptr, h->d.nu, gate);
+    toeplitz_pass(h, true, x, y, h->wx, 0.0, gate);
+  }
+}
+
+void op_copy(fde_handle h, const double* src, double* dst) {
+  const long long n = (long long)h->vec_elems();
+  k_copy<<<592, 256, 0, h->st>>>(src, dst, n);
+  FDE_CUDA(cudaGetLastError());
+  h->launches++;
+}
+
+// z = P⁻¹ r (a2)
+void op_tau(fde_handle h, const double* r, double* z, const int* gate) {
+  if (h->d.prec == FDE_PREC_NONE) {
+    op_copy(h, r, z);
+    return;
+  }
+  LineArgs a = base_args(h);
+  a.gate = gate;
+  if (h->dims == 1) {
+    a.x = r;
+    a.y = z;
+    a.nlines = h->batch;
+    a.invF = h->invF;
+    a.dpre = h->dpre;
+    a.dpost = h->dpost;
+    FDE_SWITCH_K(h->K, (launch_tau_k<KK, false>(h, a)));
+    return;
+  }
+  // 2D: rows DST (pre-scale) -> columns DST·F⁻¹·DST -> rows DST (post-scale)
+  a.nlines = h->batch * h->n;
+  a.x = r;
+  a.y = h->t1;
+  a.dpre = h->dpre;
+  FDE_SWITCH_K(h->K, (launch_dst_k<KK, false>(h, a)));
+  LineArgs b = base_args(h);
+  b.gate = gate;
+  b.nlines = h->batch * h->n;
+  b.x = h->t1;
+  b.y = h->t2;
+  b.Fx = h->Fx;
+  b.Fy = h->Fy;
+  b.fscale = h->fscale;
+  FDE_SWITCH_K(h->K, (launch_tau_k<KK, true>(h, b)));
+  LineArgs c = base_args(h);
+  c.gate = gate;
+  c.nlines = h->batch * h->n;
+  c.x = h->t2;
+  c.y = z;
+  c.dpost = h->dpost;
+  FDE_SWITCH_K(h->K, (launch_dst_k<KK, false>(h, c)));
+}
+
+// ------------------------------------------------------------- create
+void build(fde_handle h, const fde_desc* d) {
+  h->d = *d;
+  h->st = (cudaStream_t)d->stream;
+  const int n = d->n;
+  h->n = n;
+  h->m = n + 1;
+  h->dims = d->dims;
+  h->batch = d->batch;
+  h->N = d->dims == 1 ? n : n * n;
+  const int Km = ilog2_exact(h->m);
+  if (Km < 0 || Km + 1 < KMIN || Km + 1 > KMAX)
+    throw FdeFail{FDE_ERR_UNSUPPORTED, "hot path needs n+1 a power of two with 32 <= n+1 <= 4096"};
+  h->K = Km + 1;
+  h->L = 2 * h->m;
+  const int L = h->L, m = h->m, N = h->N;
+  FDE_SWITCH_K(h->K, (init_kernel_attrs<KK>()));
+
+  // fields to host (for D, means and the combined coefficient fields)
+  auto field = [&](const double* f, double c) {
+    std::vector<double> v(N, c);
+    if (f) {
+      if (is_device_ptr(f)) FDE_CUDA(cudaMemcpy(v.data(), f, N * sizeof(double), cudaMemcpyDeviceToHost));
+      else std::memcpy(v.data(), f, N * sizeof(double));
+      for (double x : v)
+        if (!(x >= 0.0) || !std::isfinite(x)) throw FdeFail{FDE_ERR_INVALID_ARG, "coefficient field has a negative or non-finite entry"};
+    }
+    return v;
+  };
+  const bool two = d->dims == 2;
+  std::vector<double> dp = field(d->dp_field, d->dp), dm = field(d->dm_field, d->dm);
+  std::vector<double> ep, em;
+  if (two) { ep = field(d->ep_field, d->ep); em = field(d->em_field, d->em); }
+  h->var_x = d->dp_field || d->dm_field;
+  h->var_y = two && (d->ep_field || d->em_field);
+  const double ywt = d->ywt > 0.0 ? d->ywt : 1.0;
+
+  // twiddles
+  std::vector<double2> tw(L / 2);
+  for (int e = 0; e < L / 2; ++e) { auto z = root_of_unity(e, L); tw[e] = make_double2(z.real(), z.imag()); }
+  h->tw = h->upload(tw);
+
+  // circulant eigenvalues λ = DFT_L(c), c = first column of the embedding
+  auto lambda = [&](double order) {
+    std::vector<double> co = stencil_coeffs(order, n + 1, d->stencil);
+    std::vector<std::complex<double>> c(L, 0.0);
+    for (int k = 0; k < n; ++k) c[k] = -co[k + 1];
+    c[L - 1] = -co[0];
+    host_fft(c);
+    return c;
+  };
+  auto make_dir = [&](double order, bool var, double cpl, double cmi, double wgt, double2*& mu, double*& lS,
+                      double*& lK, double*& cPf, double*& cMf, const std::vector<double>& fp,
+                      const std::vector<double>& fm) {
+    std::vector<std::complex<double>> lam = lambda(order);
+    const double invL = 1.0 / L;
+    if (!var) {
+      // μ = (d+ + d-) Re λ + i (d+ - d-) Im λ (constant coefficients)
+      std::vector<double2> mv(L);
+      for (int s = 0; s < L; ++s) {
+        const std::complex<double> l = lam[bitrev_host(s, h->K)];
+        mv[s] = make_double2(wgt * (cpl + cmi) * l.real() * invL, wgt * (cpl - cmi) * l.imag() * invL);
+      }
+      mu = h->upload(mv);
+    } else {
+      std::vector<double> s1(L), s2(L);
+      std::vector<double2> mv(2 * L);  // two-pass fallback multipliers
+      for (int s = 0; s < L; ++s) {
+        const std::complex<double> l = lam[bitrev_host(s, h->K)];
+        s1[s] = l.real() * invL;
+        s2[s] = l.imag() * invL;
+        mv[s] = make_double2(s1[s], 0.0);
+        mv[L + s] = make_double2(0.0, s2[s]);
+      }
+      lS = h->upload(s1);
+      lK = h->upload(s2);
+      mu = h->upload(mv);
+      std::vector<double> p(N), q(N);
+      for (int i = 0; i < N; ++i) { p[i] = wgt * (fp[i] + fm[i]); q[i] = wgt * (fp[i] - fm[i]); }
+      cPf = h->upload(p);
+      cMf = h->upload(q);
+    }
+  };
+  make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, h->mu_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm);
+  if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, h->mu_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em);
+
+  // preconditioner tables
+  const int prec = d->prec;
+  if (prec != FDE_PREC_NONE) {
+    double cx = d->cx, cy = d->cy;
+    if (prec == FDE_PREC_TAU) {
+      if (!(cx > 0.0)) {  // R12: mean((d+ + d-)/2)
+        double s = 0;
+        for (int i = 0; i < N; ++i) s += 0.5 * (dp[i] + dm[i]);
+        cx = s / N;
+      }
+      if (two && !(cy > 0.0)) {
+        double s = 0;
+        for (int i = 0; i < N; ++i) s += 0.5 * (ep[i] + em[i]);
+        cy = s / N;
+      }
+    } else {
+      if (!(cx > 0.0)) cx = 1.0;
+      if (!(cy > 0.0)) cy = 1.0;
+    }
+    h->cx = cx;
+    h->cy = two ? cy : 0.0;
+    std::vector<double> Fa(n), Fb(n);
+    for (int j = 1; j <= n; ++j) {
+      const double th = M_PI * (double)j / (double)m;
+      Fa[j - 1] = d->stencil == 1 ? symbol_p(d->alpha, th) : symbol_q(d->alpha, th);
+      if (two) Fb[j - 1] = d->stencil == 1 ? symbol_p(d->beta, th) : symbol_q(d->beta, th);
+      if (!(Fa[j - 1] > 1e-300) || (two && !(Fb[j - 1] > 1e-300)))
+        throw FdeFail{FDE_ERR_SINGULAR, "symbol sample <= 0"};
+    }
+    if (!two) {
+      std::vector<double> inv(n);
+      for (int j = 0; j < n; ++j) inv[j] = 1.0 / (cx * Fa[j]) / (2.0 * m);
+      h->invF = h->upload(inv);
+    } else {
+      for (int j = 0; j < n; ++j) { Fa[j] *= cx; Fb[j] *= cy; }
+      h->Fx = h->upload(Fa);
+      h->Fy = h->upload(Fb);
+      h->fscale = 1.0 / ((2.0 * m) * (2.0 * m));
+    }
+    if (prec == FDE_PREC_TAU_D || prec == FDE_PREC_TAU_DSYM) {
+      std::vector<double> D(N);
+      for (int i = 0; i < N; ++i) {
+        D[i] = two ? 0.25 * (dp[i] + dm[i] + ep[i] + em[i]) : 0.5 * (dp[i] + dm[i]);
+        if (!(D[i] > 0.0)) throw FdeFail{FDE_ERR_SINGULAR, "D has a zero entry (common zero of the coefficients)"};
+      }
+      std::vector<double> f(N);
+      if (prec == FDE_PREC_TAU_D) {
+        for (int i = 0; i < N; ++i) f[i] = 1.0 / D[i];
+        h->dpost = h->upload(f);
+      } else {
+        for (int i = 0; i < N; ++i) f[i] = 1.0 / std::sqrt(D[i]);
+        h->dpre = h->upload(f);
+        h->dpost = h->dpre;
+      }
+    }
+  }
+
+  const size_t ve = h->vec_elems();
+  h->wx = h->dalloc<double>(ve);
+  h->t1 = h->dalloc<double>(ve);
+  h->t2 = h->dalloc<double>(ve);
+  h->t3 = h->dalloc<double>(ve);
+  h->hin = h->dalloc<double>(ve);
+  h->hout = h->dalloc<double>(ve);
+  h->sst = h->dalloc<SolveState>(h->batch);
+  h->gsm = h->dalloc<GmresSmall>(h->batch);
+  h->ctr = h->dalloc<Counters>(1);
+  h->part = h->dalloc<double>((size_t)h->batch * (MAX_RESTART + 1) * RED_BLOCKS);
+  FDE_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->st));
+  FDE_CUDA(cudaMemsetAsync(h->sst, 0, sizeof(SolveState) * h->batch, h->st));
+  FDE_CUDA(cudaStreamSynchronize(h->st));
+}
+
+void validate(const fde_desc* d) {
+  auto bad = [](const char* m) { throw FdeFail{FDE_ERR_INVALID_ARG, m}; };
+  if (!d) bad("descriptor is NULL");
+  if (d->dims != 1 && d->dims != 2) bad("dims must be 1 or 2");
+  if (d->n < 1) bad("n must be >= 1");
+  if (d->batch < 1 || d->batch > 8) bad("batch must be in [1, 8]");
+  if (d->stencil != 1 && d->stencil != 2) bad("stencil must be 1 or 2");
+  if (!(d->alpha > 1.0 && d->alpha < 2.0)) bad("alpha must lie in (1, 2)");
+  if (d->dims == 2 && !(d->beta > 1.0 && d->beta < 2.0)) bad("beta must lie in (1, 2)");
+  if (!(d->nu >= 0.0) || !std::isfinite(d->nu)) bad("nu must be finite and >= 0");
+  auto coef = [&](double v) { if (!(v >= 0.0) || !std::isfinite(v)) bad("coefficients must be finite and >= 0"); };
+  coef(d->dp);
+  coef(d->dm);
+  if (d->dims == 2) { coef(d->ep); coef(d->em); }
+  if (d->prec < FDE_PREC_NONE || d->prec > FDE_PREC_TAU_DSYM) bad("unknown prec kind");
+  if (!std::isfinite(d->cx) || !std::isfinite(d->cy) || !std::isfinite(d->ywt)) bad("cx, cy, ywt must be finite");
+  if ((long long)d->n * (d->dims == 2 ? d->n : 1) * d->batch > (1LL << 31)) bad("problem too large");
+}
+
+fde_status fail(fde_handle h, const FdeFail& f) {
+  if (h) h->err = f.msg;
+  return f.s;
+}
+
+// staged vector in/out -------------------------------------------------------
+struct Staged {
+  fde_handle h;
+  const double* in_dev = nullptr;
+  double* out_dev = nullptr;
+  double* out_user = nullptr;
+  bool out_host = false, any_host = false;
+};
+
+const double* stage_in(fde_handle h, const double* p, double* buf, bool& host) {
+  if (is_device_ptr(p)) { host = false; return p; }
+  host = true;
+  FDE_CUDA(cudaMemcpyAsync(buf, p, h->vec_elems() * sizeof(double), cudaMemcpyHostToDevice, h->st));
+  return buf;
+}
+
+fde_status worst_status(fde_handle h, fde_stats* st_out, bool pcg) {
+  std::vector<SolveState> s(h->batch);
+  FDE_CUDA(cudaMemcpyAsync(s.data(), h->sst, sizeof(SolveState) * h->batch, cudaMemcpyDeviceToHost, h->st));
+  FDE_CUDA(cudaStreamSynchronize(h->st));
+  fde_status worst = FDE_OK;
+  for (int b = 0; b < h->batch; ++b) {
+    fde_status sb = FDE_OK;
+    if (s[b].status != ST_OK) sb = (fde_status)s[b].status;
+    else if (!s[b].converged) sb = FDE_ERR_NOT_CONVERGED;
+    if (sb != FDE_OK && (worst == FDE_OK || worst == FDE_ERR_NOT_CONVERGED)) worst = sb;
+    if (st_out) {
+      st_out[b].iters = s[b].iters;
+      st_out[b].restarts = s[b].restarts;
+      st_out[b].converged = s[b].converged;
+      st_out[b].status = sb;
+      st_out[b].rel_res = s[b].rnorm;
+    }
+  }
+  (void)pcg;
+  return worst;
+}
+
+VecArgs vec_args(fde_handle h, double rtol, int maxit, int restart, int left) {
+  VecArgs a;
+  a.N = h->N;
+  a.batch = h->batch;
+  a.st = h->sst;
+  a.gs = h->gsm;
+  a.ctr = h->ctr;
+  a.part = h->part;
+  a.rtol = rtol;
+  a.maxit = maxit;
+  a.restart = restart;
+  a.left = left;
+  return a;
+}
+
+__global__ void k_reset_counters(Counters* c, SolveState* s, int batch) {
+  if (threadIdx.x == 0) {
+    c->active = batch;
+    c->unfinished = batch;
+    for (int i = 0; i < 64; ++i) c->tickets[i] = 0u;
+  }
+  if ((int)threadIdx.x < batch) {
+    SolveState& q = s[threadIdx.x];
+    q.cyc_active = 1;
+    q.finished = 0;
+    q.converged = 0;
+    q.status = 0;
+    q.iters = 0;
+    q.kused = 0;
+    q.restarts = 0;
+  }
+}
+
+void ensure_krylov(fde_handle h, int nvecV) {
+  const size_t ve = h->vec_elems();
+  if (!h->kx) {
+    h->kx = h->dalloc<double>(ve);
+    h->kb = h->dalloc<double>(ve);
+    h->kr = h->dalloc<double>(ve);
+    h->kz = h->dalloc<double>(ve);
+    h->kp = h->dalloc<double>(ve);
+    h->kq = h->dalloc<double>(ve);
+  }
+  if (nvecV > h->V_cols) {
+    h->V = h->dalloc<double>(ve * nvecV);
+    h->V_cols = nvecV;
+  }
+}
+
+#define VGRID dim3(RED_BLOCKS, h->batch)
+
+// one PCG iteration (device-gated)
+void pcg_iteration(fde_handle h, const VecArgs& va) {
+  const int* gate = &h->ctr->active;
+  op_matvec(h, h->kp, h->kq, gate);
+  k_pcg_pq<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kp, h->kq);
+  k_pcg_xr<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kp, h->kq, h->kx, h->kr);
+  op_tau(h, h->kr, h->kz, gate);
+  k_pcg_rz<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kr, h->kz);
+  k_pcg_p<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kz, h->kp);
+  FDE_CUDA(cudaGetLastError());
+  h->launches += 4;
+}
+
+fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int maxit, fde_stats* st) {
+  ensure_krylov(h, 0);
+  bool bh = false;
+  const double* bd = stage_in(h, b, h->hin, bh);
+  const VecArgs va = vec_args(h, rtol, maxit, 0, 0);
+  k_reset_counters<<<1, 32, 0, h->st>>>(h->ctr, h->sst, h->batch);
+  k_pcg_init<<<VGRID, RED_THREADS, 0, h->st>>>(va, bd, h->kx, h->kr);
+  h->launches += 2;
+  op_tau(h, h->kr, h->kz, nullptr);
+  k_pcg_init2<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kr, h->kz, h->kp);
+  h->launches++;
+  FDE_CUDA(cudaGetLastError());
+
+  // a chunk of iterations captured once as a CUDA graph
+  const int chunk = 8;
+  if (!h->g_pcg || h->g_rtol != rtol || h->g_maxit != maxit) {
+    if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
+    cudaStream_t cs;
+    FDE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaStream_t saved = h->st;
+    h->st = cs;
+    const long long l0 = h->launches;
+    cudaGraph_t g;
+    FDE_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < chunk; ++i) pcg_iteration(h, va);
+    FDE_CUDA(cudaStreamEndCapture(cs, &g));
+    FDE_CUDA(cudaGraphInstantiate(&h->g_pcg, g, 0));
+    cudaGraphDestroy(g);
+    h->g_pcg_nodes = (int)(h->launches - l0);
+    h->launches = l0;
+    h->st = saved;
+    cudaStreamDestroy(cs);
+    h->g_rtol = rtol;
+    h->g_maxit = maxit;
+  }
+  int flag = 1;
+  int* hflag = nullptr;
+  FDE_CUDA(cudaMallocHost(&hflag, sizeof(int)));
+  for (int done = 0; done < maxit; done += chunk) {
+    FDE_CUDA(cudaGraphLaunch(h->g_pcg, h->st));
+    h->launches += h->g_pcg_nodes;
+    FDE_CUDA(cudaMemcpyAsync(hflag, &h->ctr->active, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    FDE_CUDA(cudaStreamSynchronize(h->st));
+    flag = *hflag;
+    if (flag == 0) break;
+  }
+  cudaFreeHost(hflag);
+  if (is_device_ptr(x)) {
+    FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+  } else {
+    FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  }
+  return worst_status(h, st, true);
+}
+
+// ---------------------------------------------------------------- GMRES
+void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
+  const int* gA = &h->ctr->active;
+  const int* gU = &h->ctr->unfinished;
+  const size_t vs = h->vec_elems();
+  double* V = h->V;
+  k_gm_scale<<<VGRID, RED_THREADS, 0, h->st>>>(va, V);
+  h->launches++;
+  for (int j = 0; j < restart; ++j) {
+    double* Vj = V + (size_t)j * vs;
+    double* Vn = V + (size_t)(j + 1) * vs;
+    if (!left) {
+      op_tau(h, Vj, h->kz, gA);
+      op_matvec(h, h->kz, Vn, gA);
+    } else {
+      op_matvec(h, Vj, h->kq, gA);
+      op_tau(h, h->kq, Vn, gA);
+    }
+    k_gm_mdot<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j);
+    k_gm_upd_mdot<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j);
+    k_gm_upd_norm<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j);
+    h->launches += 3;
+    if (j + 1 < restart) {
+      k_gm_scale<<<VGRID, RED_THREADS, 0, h->st>>>(va, Vn);
+      h->launches++;
+    }
+  }
+  // end of cycle: x += P⁻¹(V y) (right) or V y (left); restart residual
+  k_gm_lincomb<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, h->kp);
+  h->launches++;
+  if (!left) {
+    op_tau(h, h->kp, h->kz, gU);
+    k_gm_xupd<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kz, h->kx);
+  } else {
+    k_gm_xupd<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kp, h->kx);
+  }
+  h->launches++;
+  op_matvec(h, h->kx, h->kq, gU);
+  if (!left) {
+    k_gm_restart<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kb, h->kq, V, 0);
+  } else {
+    const long long ne = (long long)vs;
+    k_sub<<<592, 256, 0, h->st>>>(h->kb, h->kq, h->kr, ne);
+    op_tau(h, h->kr, h->kz, gU);
+    k_gm_restart<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kb, h->kz, V, 1);
+    h->launches++;
+  }
+  h->launches++;
+  FDE_CUDA(cudaGetLastError());
+}
+
+fde_status run_gmres(fde_handle h, const double* b, double* x, double rtol, int restart, int maxit, int left,
+                     fde_stats* st) {
+  ensure_krylov(h, restart + 1);
+  bool bh = false;
+  const double* bd = stage_in(h, b, h->hin, bh);
+  FDE_CUDA(cudaMemcpyAsync(h->kb, bd, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+  const VecArgs va = vec_args(h, rtol, maxit, restart, left);
+  k_reset_counters<<<1, 32, 0, h->st>>>(h->ctr, h->sst, h->batch);
+  h->launches++;
+  if (!left) {
+    k_gm_init<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kb, h->kx, h->V);
+  } else {
+    op_tau(h, h->kb, h->kz, nullptr);
+    k_gm_init<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kz, h->kx, h->V);
+  }
+  h->launches++;
+  FDE_CUDA(cudaGetLastError());
+
+  if (!h->g_gm || h->g_gm_restart != restart || h->g_gm_left != left || h->g_rtol != rtol || h->g_maxit != maxit) {
+    if (h->g_gm) { cudaGraphExecDestroy(h->g_gm); h->g_gm = nullptr; }
+    cudaStream_t cs;
+    FDE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaStream_t saved = h->st;
+    h->st = cs;
+    const long long l0 = h->launches;
+    cudaGraph_t g;
+    FDE_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    gmres_cycle(h, va, restart, left);
+    FDE_CUDA(cudaStreamEndCapture(cs, &g));
+    FDE_CUDA(cudaGraphInstantiate(&h->g_gm, g, 0));
+    cudaGraphDestroy(g);
+    h->g_gm_nodes = (int)(h->launches - l0);
+    h->launches = l0;
+    h->st = saved;
+    cudaStreamDestroy(cs);
+    h->g_gm_restart = restart;
+    h->g_gm_left = left;
+    h->g_rtol = rtol;
+    h->g_maxit = maxit;
+  }
+  int* hflag = nullptr;
+  FDE_CUDA(cudaMallocHost(&hflag, sizeof(int)));
+  const int max_cycles = maxit / restart + 2;
+  for (int c = 0; c < max_cycles; ++c) {
+    FDE_CUDA(cudaGraphLaunch(h->g_gm, h->st));
+    h->launches += h->g_gm_nodes;
+    FDE_CUDA(cudaMemcpyAsync(hflag, &h->ctr->unfinished, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    FDE_CUDA(cudaStreamSynchronize(h->st));
+    if (*hflag == 0) break;
+  }
+  cudaFreeHost(hflag);
+  if (is_device_ptr(x)) {
+    FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+  } else {
+    FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  }
+  return worst_status(h, st, false);
+}
+
+void free_handle(fde_handle h) {
+  if (!h) return;
+  if (h->st) cudaStreamSynchronize(h->st);
+  else cudaDeviceSynchronize();
+  if (h->g_pcg) cudaGraphExecDestroy(h->g_pcg);
+  if (h->g_gm) cudaGraphExecDestroy(h->g_gm);
+  for (void* p : h->allocs) cudaFree(p);
+  delete h;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+fde_status fde_create(const fde_desc* d, fde_handle* out) {
+  if (!out) return FDE_ERR_INVALID_ARG;
+  *out = nullptr;
+  fde_handle h = nullptr;
+  try {
+    validate(d);
+    h = new (std::nothrow) fde_handle_s();
+    if (!h) return FDE_ERR_OUT_OF_MEMORY;
+    build(h, d);
+    *out = h;
+    return FDE_OK;
+  } catch (const FdeFail& f) {
+    free_handle(h);
+    return f.s;
+  } catch (const std::bad_alloc&) {
+    free_handle(h);
+    return FDE_ERR_OUT_OF_MEMORY;
+  } catch (...) {
+    free_handle(h);
+    return FDE_ERR_CUDA;
+  }
+}
+
+void fde_destroy(fde_handle h) {
+  try { free_handle(h); } catch (...) {}
+}
+
+fde_status fde_matvec(fde_handle h, const double* x, double* y) {
+  if (!h) return FDE_ERR_INVALID_ARG;
+  if (!x || !y || (const void*)x == (const void*)y) { h->err = "x/y NULL or aliased"; return FDE_ERR_INVALID_ARG; }
+  try {
+    bool xh = false;
+    const double* xd = stage_in(h, x, h->hin, xh);
+    const bool yh = !is_device_ptr(y);
+    double* yd = yh ? h->hout : y;
+    op_matvec(h, xd, yd, nullptr);
+    if (yh) {
+      FDE_CUDA(cudaMemcpyAsync(y, yd, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    }
+    if (xh || yh) FDE_CUDA(cudaStreamSynchronize(h->st));
+    return FDE_OK;
+  } catch (const FdeFail& f) {
+    return fail(h, f);
+  } catch (...) {
+    return fail(h, FdeFail{FDE_ERR_CUDA, "unexpected exception"});
+  }
+}
+
+fde_status fde_tau_apply(fde_handle h, const double* r, double* z) {
+  if (!h) return FDE_ERR_INVALID_ARG;
+  if (!r || !z || (const void*)r == (const void*)z) { h->err = "r/z NULL or aliased"; return FDE_ERR_INVALID_ARG; }
+  try {
+    bool rh = false;
+    const double* rd = stage_in(h, r, h->hin, rh);
+    const bool zh = !is_device_ptr(z);
+    double* zd = zh ? h->hout : z;
+    op_tau(h, rd, zd, nullptr);
+    if (zh) {
+      FDE_CUDA(cudaMemcpyAsync(z, zd, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    }
+    if (rh || zh) FDE_CUDA(cudaStreamSynchronize(h->st));
+    return FDE_OK;
+  } catch (const FdeFail& f) {
+    return fail(h, f);
+  } catch (...) {
+    return fail(h, FdeFail{FDE_ERR_CUDA, "unexpected exception"});
+  }
+}
+
+fde_status fde_pcg(fde_handle h, const double* b, double* x, double rtol, int32_t maxit, fde_stats* st) {
+  if (!h) return FDE_ERR_INVALID_ARG;
+  if (!b || !x || (const void*)b == (const void*)x) { h->err = "b/x NULL or aliased"; return FDE_ERR_INVALID_ARG; }
+  if (!(rtol > 0.0) || maxit < 1) { h->err = "rtol must be > 0 and maxit >= 1"; return FDE_ERR_INVALID_ARG; }
+  if (h->d.prec != FDE_PREC_NONE && h->d.prec != FDE_PREC_TAU) {
+    h->err = "PCG needs a symmetric preconditioner (NONE or TAU)";
+    return FDE_ERR_INVALID_ARG;
+  }
+  try {
+    return run_pcg(h, b, x, rtol, maxit, st);
+  } catch (const FdeFail& f) {
+    return fail(h, f);
+  } catch (...) {
+    return fail(h, FdeFail{FDE_ERR_CUDA, "unexpected exception"});
+  }
+}
+
+fde_status fde_gmres(fde_handle h, const double* b, double* x, double rtol, int32_t restart, int32_t maxit,
+                     int32_t left, fde_stats* st) {
+  if (!h) return FDE_ERR_INVALID_ARG;
+  if (!b || !x || (const void*)b == (const void*)x) { h->err = "b/x NULL or aliased"; return FDE_ERR_INVALID_ARG; }
+  if (!(rtol > 0.0) || maxit < 1 || restart < 1 || restart > MAX_RESTART || (left != 0 && left != 1)) {
+    h->err = "rtol > 0, maxit >= 1, 1 <= restart <= 64, left in {0,1}";
+    return FDE_ERR_INVALID_ARG;
+  }
+  try {
+    return run_gmres(h, b, x, rtol, restart, maxit, left, st);
+  } catch (const FdeFail& f) {
+    return fail(h, f);
+  } catch (...) {
+    return fail(h, FdeFail{FDE_ERR_CUDA, "unexpected exception"});
+  }
+}
+
+const char* fde_status_str(fde_status s) {
+  switch (s) {
+    case FDE_OK: return "FDE_OK";
+    case FDE_ERR_INVALID_ARG: return "FDE_ERR_INVALID_ARG";
+    case FDE_ERR_UNSUPPORTED: return "FDE_ERR_UNSUPPORTED";
+    case FDE_ERR_OUT_OF_MEMORY: return "FDE_ERR_OUT_OF_MEMORY";
+    case FDE_ERR_CUDA: return "FDE_ERR_CUDA";
+    case FDE_ERR_SINGULAR: return "FDE_ERR_SINGULAR";
+    case FDE_ERR_NOT_SPD: return "FDE_ERR_NOT_SPD";
+    case FDE_ERR_BREAKDOWN: return "FDE_ERR_BREAKDOWN";
+    case FDE_ERR_NONFINITE: return "FDE_ERR_NONFINITE";
+    case FDE_ERR_NOT_CONVERGED: return "FDE_ERR_NOT_CONVERGED";
+  }
+  return "FDE_ERR_UNKNOWN";
+}
+
+const char* fde_last_error(fde_handle h) { return h ? h->err.c_str() : "NULL handle"; }
+
+int64_t fde_kernel_launches(fde_handle h) { return h ? (int64_t)h->launches : 0; }
+
+}  // extern "C"

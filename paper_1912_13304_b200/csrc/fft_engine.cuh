@@ -1,0 +1,243 @@
+// fp64 in-place FFT engine for one line-transform per "FFT group" of threads.
+//
+// L = 2^K complex points, each of the P = L/R threads of a group holds R = 2^k
+// points in registers. A DIF chain (natural order in -> bit-reversed order
+// out) is a sequence of passes from the top bits down; each pass does an
+// R-point DFT in registers (radix-2 stages with compile-time roots of unity)
+// followed by one general twiddle per point, and hands its points to the next
+// pass through shared memory (one barrier per exchange). The DIT chain is the
+// exact mirror (bit-reversed in -> natural out), so a DIF chain, a pointwise
+// product in bit-reversed order and a DIT chain form a convolution without any
+// explicit bit-reversal permutation. The pass/twiddle bookkeeping is checked
+// against numpy.fft in tools/fft_engine_model.py.
+//
+// Pass i (0 = top): active bits [lo_i, lo_i + ka_i); a thread's R local points
+// sit at positions ((t >> lo) << (lo + k)) | (q << lo) | (t & (2^lo - 1)).
+// Post-twiddle (DIF) / pre-twiddle (DIT) for local q is
+// W_L^{sigma * t_lo * bitrev_ka(q) * 2^(K - lo - ka)}, generated from one base
+// twiddle loaded from the table tw[e] = exp(-2 pi i e / L), e < L/2.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fde {
+
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 c_conj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 c_scale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// a * exp(SIGMA * 2 pi i * e / N) for a compile-time-resolvable (after unrolling) e, N <= 16.
+template <int SIGMA>
+__device__ __forceinline__ double2 c_root(double2 a, int e, int N) {
+  // reduce to 16ths
+  const int e16 = (e * (16 / N)) & 15;
+  constexpr double C1 = 0.92387953251128675613;  // cos(pi/8)
+  constexpr double S1 = 0.38268343236508977173;  // sin(pi/8)
+  constexpr double R2 = 0.70710678118654752440;  // cos(pi/4)
+  const double s = (double)SIGMA;
+  switch (e16) {
+    case 0: return a;
+    case 4: return make_double2(-s * a.y, s * a.x);            // * (s i)
+    case 8: return make_double2(-a.x, -a.y);
+    case 12: return make_double2(s * a.y, -s * a.x);           // * (-s i)
+    case 2: return make_double2(R2 * (a.x - s * a.y), R2 * (a.y + s * a.x));
+    case 6: return make_double2(R2 * (-a.x - s * a.y), R2 * (-a.y + s * a.x));
+    case 10: return make_double2(R2 * (-a.x + s * a.y), R2 * (-a.y - s * a.x));
+    case 14: return make_double2(R2 * (a.x + s * a.y), R2 * (a.y - s * a.x));
+    default: {
+      // general 16th root: angle = e16 * pi / 8
+      const int oct = e16 >> 1;  // 0..7 eighth-turn; e16 odd here
+      double c, sn;
+      // cos/sin of (2*oct+1) * pi/8 for oct = 0..7
+      switch (oct) {
+        case 0: c = C1; sn = S1; break;
+        case 1: c = S1; sn = C1; break;
+        case 2: c = -S1; sn = C1; break;
+        case 3: c = -C1; sn = S1; break;
+        case 4: c = -C1; sn = -S1; break;
+        case 5: c = -S1; sn = -C1; break;
+        case 6: c = S1; sn = -C1; break;
+        default: c = C1; sn = -S1; break;
+      }
+      return c_mul(a, make_double2(c, s * sn));
+    }
+  }
+}
+
+__host__ __device__ constexpr int ceil_div_c(int a, int b) { return (a + b - 1) / b; }
+
+template <int K_, int k_>
+struct FftGeom {
+  static constexpr int K = K_, k = k_;
+  static constexpr int L = 1 << K, R = 1 << k, P = L >> k;
+  static constexpr int NP = ceil_div_c(K, k);
+  static constexpr int PAD_SHIFT = 4;  // one 16-byte pad slot per 16 points
+  static constexpr int SM_STRIDE = L + (L >> PAD_SHIFT) + 2;  // per-group smem stride (double2)
+  __host__ __device__ static constexpr int lo(int i) { return K - (i + 1) * k > 0 ? K - (i + 1) * k : 0; }
+  __host__ __device__ static constexpr int ka(int i) { return K - i * k - lo(i); }
+  __device__ __forceinline__ static int pos(int t, int i, int q) {
+    const int l = lo(i);
+    return ((t >> l) << (l + k)) | (q << l) | (t & ((1 << l) - 1));
+  }
+  __device__ __forceinline__ static int phys(int p) { return p + (p >> PAD_SHIFT); }
+};
+
+__device__ __forceinline__ int bitrev_dev(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }
+__host__ __device__ constexpr int bitrev_c(int x, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) { r = (r << 1) | (x & 1); x >>= 1; }
+  return r;
+}
+
+// R-point DIF DFT over the `ka` low local bits (in-place, output bit-reversed).
+template <int k, int ka, int SIGMA>
+__device__ __forceinline__ void dft_dif(double2 (&v)[1 << k]) {
+#pragma unroll
+  for (int j = ka - 1; j >= 0; --j) {
+#pragma unroll
+    for (int q = 0; q < (1 << k); ++q) {
+      if (q & (1 << j)) continue;
+      const int q2 = q | (1 << j);
+      double2 a = v[q], b = v[q2];
+      v[q] = c_add(a, b);
+      v[q2] = c_root<SIGMA>(c_sub(a, b), q & ((1 << j) - 1), 1 << (j + 1));
+    }
+  }
+}
+
+// mirror of dft_dif<-SIGMA>: bit-reversed in, natural out, unnormalised.
+template <int k, int ka, int SIGMA>
+__device__ __forceinline__ void dft_dit(double2 (&v)[1 << k]) {
+#pragma unroll
+  for (int j = 0; j < ka; ++j) {
+#pragma unroll
+    for (int q = 0; q < (1 << k); ++q) {
+      if (q & (1 << j)) continue;
+      const int q2 = q | (1 << j);
+      double2 a = v[q];
+      double2 b = c_root<SIGMA>(v[q2], q & ((1 << j) - 1), 1 << (j + 1));
+      v[q] = c_add(a, b);
+      v[q2] = c_sub(a, b);
+    }
+  }
+}
+
+// multiply v[q] by w^{bitrev_ka(q)} for the active-q range (q < 2^ka); w = base twiddle.
+template <int k, int ka>
+__device__ __forceinline__ void apply_twiddles(double2 (&v)[1 << k], double2 w) {
+  constexpr int RA = 1 << ka;
+  double2 pw[RA];
+  pw[0] = make_double2(1.0, 0.0);
+  pw[1] = w;
+#pragma unroll
+  for (int r = 2; r < RA; ++r) pw[r] = c_mul(pw[r >> 1], pw[r - (r >> 1)]);
+#pragma unroll
+  for (int q = 1; q < RA; ++q) v[q] = c_mul(v[q], pw[bitrev_c(q, ka)]);
+}
+
+template <class G, int I, int SIGMA>
+__device__ __forceinline__ double2 base_twiddle(int t, const double2* __restrict__ tw) {
+  constexpr int l = G::lo(I), a = G::ka(I);
+  const int tlo = t & ((1 << l) - 1);
+  const double2 w = __ldg(&tw[tlo << (G::K - l - a)]);
+  return SIGMA < 0 ? w : c_conj(w);
+}
+
+// DIF pass I on registers (no memory traffic).
+template <class G, int I, int SIGMA, bool HALF_ZERO>
+__device__ __forceinline__ void dif_pass(double2 (&v)[G::R], int t, const double2* __restrict__ tw) {
+  constexpr int a = G::ka(I);
+  if (HALF_ZERO && a == G::k) {
+    // upper half of the inputs are zero: first radix-2 stage is a copy/twiddle
+    constexpr int j = G::k - 1;
+#pragma unroll
+    for (int q = 0; q < (1 << j); ++q) v[q | (1 << j)] = c_root<SIGMA>(v[q], q, 1 << (j + 1));
+    // remaining stages
+#pragma unroll
+    for (int jj = j - 1; jj >= 0; --jj) {
+#pragma unroll
+      for (int q = 0; q < G::R; ++q) {
+        if (q & (1 << jj)) continue;
+        const int q2 = q | (1 << jj);
+        double2 x = v[q], y = v[q2];
+        v[q] = c_add(x, y);
+        v[q2] = c_root<SIGMA>(c_sub(x, y), q & ((1 << jj) - 1), 1 << (jj + 1));
+      }
+    }
+  } else {
+    dft_dif<G::k, a, SIGMA>(v);
+  }
+  if (G::lo(I) > 0) apply_twiddles<G::k, a>(v, base_twiddle<G, I, SIGMA>(t, tw));
+}
+
+template <class G, int I, int SIGMA>
+__device__ __forceinline__ void dit_pass(double2 (&v)[G::R], int t, const double2* __restrict__ tw) {
+  constexpr int a = G::ka(I);
+  if (G::lo(I) > 0) apply_twiddles<G::k, a>(v, base_twiddle<G, I, SIGMA>(t, tw));
+  dft_dit<G::k, a, SIGMA>(v);
+}
+
+template <class G>
+__device__ __forceinline__ void sm_store(double2* sm, const double2 (&v)[G::R], int t, int i) {
+#pragma unroll
+  for (int q = 0; q < G::R; ++q) sm[G::phys(G::pos(t, i, q))] = v[q];
+}
+template <class G>
+__device__ __forceinline__ void sm_load(const double2* sm, double2 (&v)[G::R], int t, int i) {
+#pragma unroll
+  for (int q = 0; q < G::R; ++q) v[q] = sm[G::phys(G::pos(t, i, q))];
+}
+
+// Helper to unroll passes with compile-time indices.
+template <class G, int I, int SIGMA, bool HALF_ZERO>
+struct DifChain {
+  __device__ __forceinline__ static void run(double2 (&v)[G::R], double2* sm, int t, const double2* __restrict__ tw) {
+    if (I > 0) {
+      sm_store<G>(sm, v, t, I - 1);
+      __syncthreads();
+      sm_load<G>(sm, v, t, I);
+    }
+    dif_pass<G, I, SIGMA, (I == 0) && HALF_ZERO>(v, t, tw);
+    DifChain<G, I + 1, SIGMA, HALF_ZERO>::run(v, sm, t, tw);
+  }
+};
+template <class G, int SIGMA, bool HALF_ZERO>
+struct DifChain<G, G::NP, SIGMA, HALF_ZERO> {
+  __device__ __forceinline__ static void run(double2 (&)[G::R], double2*, int, const double2* __restrict__) {}
+};
+
+template <class G, int I, int SIGMA>
+struct DitChain {  // runs passes I, I-1, ..., 0
+  __device__ __forceinline__ static void run(double2 (&v)[G::R], double2* sm, int t, const double2* __restrict__ tw) {
+    if (I < G::NP - 1) {
+      sm_store<G>(sm, v, t, I + 1);
+      __syncthreads();
+      sm_load<G>(sm, v, t, I);
+    }
+    dit_pass<G, I, SIGMA>(v, t, tw);
+    DitChain<G, I - 1, SIGMA>::run(v, sm, t, tw);
+  }
+};
+template <class G, int SIGMA>
+struct DitChain<G, -1, SIGMA> {
+  __device__ __forceinline__ static void run(double2 (&)[G::R], double2*, int, const double2* __restrict__) {}
+};
+
+// Full chains. v enters holding pass-0 inputs (DIF) / pass-(NP-1) inputs (DIT)
+// and leaves holding pass-(NP-1) outputs (DIF; positions (t<<k)|q, bit-reversed
+// frequency order) / pass-0 outputs (DIT; positions (q<<(K-k))|t, natural order).
+// Every thread of the CTA must call these (they contain __syncthreads).
+template <class G, int SIGMA, bool HALF_ZERO>
+__device__ __forceinline__ void dif_chain(double2 (&v)[G::R], double2* sm, int t, const double2* __restrict__ tw) {
+  DifChain<G, 0, SIGMA, HALF_ZERO>::run(v, sm, t, tw);
+}
+template <class G, int SIGMA>
+__device__ __forceinline__ void dit_chain(double2 (&v)[G::R], double2* sm, int t, const double2* __restrict__ tw) {
+  DitChain<G, G::NP - 1, SIGMA>::run(v, sm, t, tw);
+}
+
+}  // namespace fde

@@ -1,0 +1,579 @@
+// Krylov vector kernels: fused axpys and dot products
+// with deterministic two-stage reductions, and the small per-RHS scalar logic
+// (PCG α/β, GMRES CGS2 + Givens) executed on the device by the last block of
+// each reduction, so a whole solve runs without host round trips.
+//
+// Reduction layout: every kernel runs on a grid (RED_BLOCKS, batch); block
+// (bx, b) writes its partial sums to part[(b*nvec + i)*RED_BLOCKS + bx];
+// the last block to arrive (atomic ticket per RHS) sums the partials in
+// fixed order with one warp per vector, so results are bitwise
+// reproducible (no fp64 atomics).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fde {
+
+constexpr int RED_BLOCKS = 296;   // 2 x 148 SMs
+constexpr int RED_THREADS = 256;
+constexpr int MAX_RESTART = 64;
+
+enum { ST_OK = 0, ST_NOT_SPD = 6, ST_BREAKDOWN = 7, ST_NONFINITE = 8 };
+
+struct SolveState {          // one per RHS, device resident
+  double bnorm;              // ‖b‖ (right/PCG) or ‖P⁻¹b‖ (left GMRES): the tolerance reference
+  double beta;               // GMRES: current cycle's ‖r‖; PCG: unused
+  double rho, alpha, betac;  // PCG scalars
+  double rnorm;              // last residual estimate
+  double inv_h;              // GMRES: 1/H[j+1,j] of the last step (normalisation)
+  int iters;                 // matvecs (PCG) / Arnoldi steps (GMRES)
+  int cyc_active;            // GMRES: still stepping in this cycle; PCG: still iterating
+  int finished;              // solution final
+  int converged;
+  int status;                // ST_*
+  int kused;                 // GMRES: steps taken in the current cycle
+  int restarts;
+  int pad;
+};
+
+struct GmresSmall {          // one per RHS
+  double H[(MAX_RESTART + 1) * MAX_RESTART];   // column-major: H[i + j*(MAX_RESTART+1)]
+  double cs[MAX_RESTART], sn[MAX_RESTART], g[MAX_RESTART + 1];
+  double h[MAX_RESTART + 1];                   // CGS pass 1 coefficients
+  double h2[MAX_RESTART + 1];                  // CGS pass 2 coefficients
+  double y[MAX_RESTART];
+};
+
+struct Counters {            // device counters
+  int active;                // # RHS with cyc_active (gates Arnoldi/PCG kernels)
+  int unfinished;            // # RHS not finished (gates end-of-cycle kernels)
+  unsigned tickets[64];      // per-RHS last-block tickets (batch <= 8, 8 slots each)
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-wide sum of NV values; result valid in thread 0. red: smem [NV][32]
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&acc)[NV], double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double v = warp_sum(acc[i]);
+    if (lane == 0) red[i * 32 + wid] = v;
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double v = lane < nw ? red[i * 32 + lane] : 0.0;
+      acc[i] = warp_sum(v);
+    }
+  }
+  __syncthreads();
+}
+
+// ticket: returns true in all threads of the last block (per RHS b) to finish
+__device__ __forceinline__ bool last_block(unsigned* ticket) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+  return s_last;
+}
+
+// last block: out[i] = sum_bx part[(i)*RED_BLOCKS + bx] in fixed order (one warp per vector)
+__device__ __forceinline__ void finalize(const double* part, int nvec, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < nvec; i += nw) {
+    double s = 0.0;
+    for (int bx = lane; bx < RED_BLOCKS; bx += 32) s += __ldcg(part + (size_t)i * RED_BLOCKS + bx);
+    s = warp_sum(s);
+    if (lane == 0) out[i] = s;
+  }
+  __syncthreads();
+}
+
+struct VecArgs {
+  int N;                 // elements per RHS
+  int batch;
+  SolveState* st;
+  GmresSmall* gs;
+  Counters* ctr;
+  double* part;          // partial sums [batch][nvec][RED_BLOCKS]
+  double rtol;
+  int maxit;
+  int restart;
+  int left;
+};
+
+#define FDE_GRID_LOOP(e) for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x)
+
+__device__ __forceinline__ void mark_finished(VecArgs& a, SolveState& s) {
+  if (s.cyc_active) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
+  if (!s.finished) { s.finished = 1; atomicSub(&a.ctr->unfinished, 1); }
+}
+
+// ============================================================ PCG (a3) ====
+// init: x = 0, r = b; ‖b‖
+__global__ void k_pcg_init(VecArgs a, const double* __restrict__ b, double* x, double* r) {
+  const int rb = blockIdx.y, N = a.N;
+  const size_t o = (size_t)rb * N;
+  double acc[1] = {0.0};
+  FDE_GRID_LOOP(e) {
+    const double v = b[o + e];
+    x[o + e] = 0.0;
+    r[o + e] = v;
+    acc[0] = fma(v, v, acc[0]);
+  }
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  double* part = a.part + (size_t)rb * RED_BLOCKS;
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    __shared__ double out[1];
+    finalize(part, 1, out);
+    if (threadIdx.x == 0) {
+      SolveState& s = a.st[rb];
+      s.bnorm = sqrt(out[0]);
+      s.iters = 0;
+      s.converged = 0;
+      s.status = ST_OK;
+      s.restarts = 0;
+      s.rnorm = 1.0;
+      if (!(s.bnorm > 0.0)) {  // b = 0 -> x = 0 (or NaN input)
+        s.converged = (s.bnorm == 0.0);
+        if (!(s.bnorm == 0.0)) s.status = ST_NONFINITE;
+        s.rnorm = 0.0;
+        mark_finished(a, s);
+      }
+    }
+  }
+}
+
+// p = z; rho = r·z
+__global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const double* __restrict__ z, double* p) {
+  const int rb = blockIdx.y, N = a.N;
+  const size_t o = (size_t)rb * N;
+  double acc[1] = {0.0};
+  FDE_GRID_LOOP(e) {
+    const double zv = z[o + e];
+    p[o + e] = zv;
+    acc[0] = fma(r[o + e], zv, acc[0]);
+  }
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  double* part = a.part + (size_t)rb * RED_BLOCKS;
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    __shared__ double out[1];
+    finalize(part, 1, out);
+    if (threadIdx.x == 0) {
+      SolveState& s = a.st[rb];
+      s.rho = out[0];
+      if (s.cyc_active && !(s.rho > 0.0)) {
+        s.status = isfinite(s.rho) ? ST_NOT_SPD : ST_NONFINITE;
+        mark_finished(a, s);
+      }
+    }
+  }
+}
+
+// α = ρ / (p·q)
+__global__ void k_pcg_pq(VecArgs a, const double* __restrict__ p, const double* __restrict__ q) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  double acc[1] = {0.0};
+  FDE_GRID_LOOP(e) acc[0] = fma(p[o + e], q[o + e], acc[0]);
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  double* part = a.part + (size_t)rb * RED_BLOCKS;
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    __shared__ double out[1];
+    finalize(part, 1, out);
+    if (threadIdx.x == 0) {
+      SolveState& s = a.st[rb];
+      const double pq = out[0];
+      if (!(pq > 0.0)) {
+        s.status = isfinite(pq) ? ST_NOT_SPD : ST_NONFINITE;
+        mark_finished(a, s);
+      } else {
+        s.alpha = s.rho / pq;
+      }
+    }
+  }
+}
+
+// x += α p ; r -= α q ; ‖r‖ ; convergence (‖r‖ <= rtol ‖b‖, R10)
+__global__ void k_pcg_xr(VecArgs a, const double* __restrict__ p, const double* __restrict__ q, double* x, double* r) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const double al = a.st[rb].alpha;
+  const size_t o = (size_t)rb * N;
+  double acc[1] = {0.0};
+  FDE_GRID_LOOP(e) {
+    x[o + e] = fma(al, p[o + e], x[o + e]);
+    const double rv = fma(-al, q[o + e], r[o + e]);
+    r[o + e] = rv;
+    acc[0] = fma(rv, rv, acc[0]);
+  }
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  double* part = a.part + (size_t)rb * RED_BLOCKS;
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    __shared__ double out[1];
+    finalize(part, 1, out);
+    if (threadIdx.x == 0) {
+      SolveState& s = a.st[rb];
+      const double rn = sqrt(out[0]);
+      s.iters += 1;
+      s.rnorm = rn / s.bnorm;
+      if (!isfinite(rn)) {
+        s.status = ST_NONFINITE;
+        mark_finished(a, s);
+      } else if (rn <= a.rtol * s.bnorm) {
+        s.converged = 1;
+        mark_finished(a, s);
+      } else if (s.iters >= a.maxit) {
+        mark_finished(a, s);
+      }
+    }
+  }
+}
+
+// ρ' = r·z ; β = ρ'/ρ ; p = z + β p is done by k_pcg_p
+__global__ void k_pcg_rz(VecArgs a, const double* __restrict__ r, const double* __restrict__ z) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  double acc[1] = {0.0};
+  FDE_GRID_LOOP(e) acc[0] = fma(r[o + e], z[o + e], acc[0]);
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  double* part = a.part + (size_t)rb * RED_BLOCKS;
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    __shared__ double out[1];
+    finalize(part, 1, out);
+    if (threadIdx.x == 0) {
+      SolveState& s = a.st[rb];
+      const double rho_new = out[0];
+      if (!(rho_new > 0.0)) {
+        s.status = isfinite(rho_new) ? ST_NOT_SPD : ST_NONFINITE;
+        mark_finished(a, s);
+      } else {
+        s.betac = rho_new / s.rho;
+        s.rho = rho_new;
+      }
+    }
+  }
+}
+
+__global__ void k_pcg_p(VecArgs a, const double* __restrict__ z, double* p) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const double be = a.st[rb].betac;
+  const size_t o = (size_t)rb * N;
+  FDE_GRID_LOOP(e) p[o + e] = fma(be, p[o + e], z[o + e]);
+}
+
+// ========================================================== GMRES (a4) ====
+// init: x = 0, r = b (right) ; ref = ‖r‖ ; V0 = r/‖r‖ (done by k_gm_scale)
+// For left preconditioning the caller passes r = P⁻¹b as `src`.
+__global__ void k_gm_init(VecArgs a, const double* __restrict__ src, double* x, double* V0) {
+  const int rb = blockIdx.y, N = a.N;
+  const size_t o = (size_t)rb * N;
+  double acc[1] = {0.0};
+  FDE_GRID_LOOP(e) {
+    const double v = src[o + e];
+    x[o + e] = 0.0;
+    V0[o + e] = v;
+    acc[0] = fma(v, v, acc[0]);
+  }
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  double* part = a.part + (size_t)rb * RED_BLOCKS;
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    __shared__ double out[1];
+    finalize(part, 1, out);
+    if (threadIdx.x == 0) {
+      SolveState& s = a.st[rb];
+      s.bnorm = sqrt(out[0]);
+      s.beta = s.bnorm;
+      s.iters = 0;
+      s.kused = 0;
+      s.restarts = 0;
+      s.converged = 0;
+      s.status = ST_OK;
+      s.rnorm = 1.0;
+      s.inv_h = 1.0 / s.beta;
+      GmresSmall& gs = a.gs[rb];
+      gs.g[0] = s.beta;
+      if (!(s.bnorm > 0.0)) {
+        s.converged = (s.bnorm == 0.0);
+        if (!(s.bnorm == 0.0)) s.status = ST_NONFINITE;
+        s.rnorm = 0.0;
+        mark_finished(a, s);
+      }
+    }
+  }
+}
+
+// V_j *= inv_h (normalise the new basis vector in place)
+__global__ void k_gm_scale(VecArgs a, double* Vj) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const double s = a.st[rb].inv_h;
+  const size_t o = (size_t)rb * N;
+  FDE_GRID_LOOP(e) Vj[o + e] *= s;
+}
+
+// Vectors of the basis: V + i*vstride + rb*N
+template <int CH>
+__device__ __forceinline__ void mdot_chunk(const double* __restrict__ V, size_t vstride, int i0, int cnt,
+                                           const double* __restrict__ w, size_t o, int N, double (&acc)[CH]) {
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c] = 0.0;
+  FDE_GRID_LOOP(e) {
+    const double wv = w[o + e];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (c < cnt) acc[c] = fma(__ldg(V + (size_t)(i0 + c) * vstride + o + e), wv, acc[c]);
+  }
+}
+
+constexpr int MD_CH = 8;
+
+// CGS pass 1: h_i = V_iᵀ w, i = 0..j
+__global__ void k_gm_mdot(VecArgs a, const double* __restrict__ V, size_t vstride, const double* __restrict__ w, int j) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  const int nv = j + 1;
+  __shared__ double red[MD_CH * 32];
+  double* part = a.part + (size_t)rb * (MAX_RESTART + 1) * RED_BLOCKS;
+  for (int i0 = 0; i0 < nv; i0 += MD_CH) {
+    double acc[MD_CH];
+    mdot_chunk<MD_CH>(V, vstride, i0, min(MD_CH, nv - i0), w, o, N, acc);
+    block_sum<MD_CH>(acc, red);
+    if (threadIdx.x == 0)
+      for (int c = 0; c < MD_CH && i0 + c < nv; ++c) part[(size_t)(i0 + c) * RED_BLOCKS + blockIdx.x] = acc[c];
+  }
+  if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, a.gs[rb].h);
+}
+
+// CGS pass 1 update + pass 2 dots: w -= V h ; h2_i = V_iᵀ w
+__global__ void k_gm_upd_mdot(VecArgs a, const double* __restrict__ V, size_t vstride, double* w, int j) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  const int nv = j + 1;
+  __shared__ double hs[MAX_RESTART + 1];
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = __ldcg(&a.gs[rb].h[i]);
+  __syncthreads();
+  FDE_GRID_LOOP(e) {
+    double wv = w[o + e];
+    for (int i = 0; i < nv; ++i) wv = fma(-hs[i], __ldg(V + (size_t)i * vstride + o + e), wv);
+    w[o + e] = wv;
+  }
+  __shared__ double red[MD_CH * 32];
+  double* part = a.part + (size_t)rb * (MAX_RESTART + 1) * RED_BLOCKS;
+  for (int i0 = 0; i0 < nv; i0 += MD_CH) {
+    double acc[MD_CH];
+    mdot_chunk<MD_CH>(V, vstride, i0, min(MD_CH, nv - i0), w, o, N, acc);
+    block_sum<MD_CH>(acc, red);
+    if (threadIdx.x == 0)
+      for (int c = 0; c < MD_CH && i0 + c < nv; ++c) part[(size_t)(i0 + c) * RED_BLOCKS + blockIdx.x] = acc[c];
+  }
+  if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, a.gs[rb].h2);
+}
+
+// CGS pass 2 update + norm + Arnoldi/Givens step (thread 0 of the last block)
+__global__ void k_gm_upd_norm(VecArgs a, const double* __restrict__ V, size_t vstride, double* w, int j) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  const int nv = j + 1;
+  __shared__ double hs[MAX_RESTART + 1];
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = __ldcg(&a.gs[rb].h2[i]);
+  __syncthreads();
+  double acc[1] = {0.0};
+  FDE_GRID_LOOP(e) {
+    double wv = w[o + e];
+    for (int i = 0; i < nv; ++i) wv = fma(-hs[i], __ldg(V + (size_t)i * vstride + o + e), wv);
+    w[o + e] = wv;
+    acc[0] = fma(wv, wv, acc[0]);
+  }
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  double* part = a.part + (size_t)rb * (MAX_RESTART + 1) * RED_BLOCKS;
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    __shared__ double out[1];
+    finalize(part, 1, out);
+    if (threadIdx.x == 0) {
+      SolveState& s = a.st[rb];
+      GmresSmall& gs = a.gs[rb];
+      constexpr int LD = MAX_RESTART + 1;
+      double* Hc = gs.H + (size_t)j * LD;
+      for (int i = 0; i <= j; ++i) Hc[i] = gs.h[i] + gs.h2[i];
+      const double hn = sqrt(out[0]);
+      Hc[j + 1] = hn;
+      for (int i = 0; i < j; ++i) {
+        const double t = gs.cs[i] * Hc[i] + gs.sn[i] * Hc[i + 1];
+        Hc[i + 1] = -gs.sn[i] * Hc[i] + gs.cs[i] * Hc[i + 1];
+        Hc[i] = t;
+      }
+      const double den = hypot(Hc[j], Hc[j + 1]);
+      gs.cs[j] = Hc[j] / den;
+      gs.sn[j] = Hc[j + 1] / den;
+      Hc[j] = den;
+      Hc[j + 1] = 0.0;
+      gs.g[j + 1] = -gs.sn[j] * gs.g[j];
+      gs.g[j] = gs.cs[j] * gs.g[j];
+      s.iters += 1;
+      s.kused = j + 1;
+      s.rnorm = fabs(gs.g[j + 1]) / s.bnorm;
+      s.inv_h = 1.0 / hn;
+      bool stop = false;
+      if (!isfinite(hn) || !isfinite(den)) {
+        s.status = ST_NONFINITE;
+        stop = true;
+      } else if (fabs(gs.g[j + 1]) <= a.rtol * s.bnorm) {
+        s.converged = 1;
+        stop = true;
+      } else if (hn == 0.0) {
+        s.status = ST_BREAKDOWN;
+        stop = true;
+      } else if (s.iters >= a.maxit || j + 1 >= a.restart) {
+        stop = true;  // end of cycle (or of the budget)
+      }
+      if (stop && s.cyc_active) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
+    }
+  }
+}
+
+// end of cycle, step 1: y = R⁻¹ g (redundantly per block), u = Σ y_i V_i
+__global__ void k_gm_lincomb(VecArgs a, const double* __restrict__ V, size_t vstride, double* u) {
+  if (a.ctr->unfinished == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (a.st[rb].finished) return;
+  const size_t o = (size_t)rb * N;
+  __shared__ double ys[MAX_RESTART];
+  const int ku = a.st[rb].kused;
+  if (threadIdx.x == 0) {
+    const GmresSmall& gs = a.gs[rb];
+    constexpr int LD = MAX_RESTART + 1;
+    for (int i = ku - 1; i >= 0; --i) {
+      double acc = gs.g[i];
+      for (int c = i + 1; c < ku; ++c) acc -= gs.H[i + (size_t)c * LD] * ys[c];
+      ys[i] = acc / gs.H[i + (size_t)i * LD];
+    }
+  }
+  __syncthreads();
+  FDE_GRID_LOOP(e) {
+    double acc = 0.0;
+    for (int i = 0; i < ku; ++i) acc = fma(ys[i], __ldg(V + (size_t)i * vstride + o + e), acc);
+    u[o + e] = acc;
+  }
+}
+
+// end of cycle, step 2: x += z
+__global__ void k_gm_xupd(VecArgs a, const double* __restrict__ z, double* x) {
+  if (a.ctr->unfinished == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (a.st[rb].finished) return;
+  const size_t o = (size_t)rb * N;
+  FDE_GRID_LOOP(e) x[o + e] += z[o + e];
+}
+
+// end of cycle, step 3 (after the caller recomputed t = A x and, for left
+// preconditioning, t = P⁻¹(b - A x) into `res`): finish or restart.
+//   right: V0 = b - t ; left: V0 = res (already the preconditioned residual)
+__global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const double* __restrict__ t, double* V0,
+                             int res_ready) {
+  if (a.ctr->unfinished == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  SolveState& s0 = a.st[rb];
+  if (s0.finished) return;
+  const bool done_now = s0.converged || s0.status != ST_OK || s0.iters >= a.maxit;
+  const size_t o = (size_t)rb * N;
+  double acc[1] = {0.0};
+  if (!done_now) {
+    FDE_GRID_LOOP(e) {
+      const double r = res_ready ? t[o + e] : b[o + e] - t[o + e];
+      V0[o + e] = r;
+      acc[0] = fma(r, r, acc[0]);
+    }
+  }
+  __shared__ double red[32];
+  block_sum<1>(acc, red);
+  double* part = a.part + (size_t)rb * (MAX_RESTART + 1) * RED_BLOCKS;
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    __shared__ double out[1];
+    finalize(part, 1, out);
+    if (threadIdx.x == 0) {
+      SolveState& s = a.st[rb];
+      if (done_now) {
+        mark_finished(a, s);
+      } else {
+        const double be = sqrt(out[0]);
+        s.beta = be;
+        s.rnorm = be / s.bnorm;
+        s.restarts += 1;
+        if (be <= a.rtol * s.bnorm) {
+          s.converged = 1;
+          mark_finished(a, s);
+        } else if (!isfinite(be)) {
+          s.status = ST_NONFINITE;
+          mark_finished(a, s);
+        } else {
+          s.inv_h = 1.0 / be;
+          s.kused = 0;
+          a.gs[rb].g[0] = be;
+          if (!s.cyc_active) { s.cyc_active = 1; atomicAdd(&a.ctr->active, 1); }
+        }
+      }
+    }
+  }
+}
+
+// plain helpers -------------------------------------------------------------
+__global__ void k_copy(const double* __restrict__ src, double* dst, long long n) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+}
+__global__ void k_sub(const double* __restrict__ b, const double* __restrict__ t, double* r, long long n) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    r[e] = b[e] - t[e];
+}
+__global__ void k_scale_field(const double* __restrict__ src, const double* __restrict__ f, double* dst, int N, long long n) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    dst[e] = src[e] * f[e % N];
+}
+
+}  // namespace fde

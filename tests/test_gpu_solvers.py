@@ -1,0 +1,121 @@
+"""GPU parity of the Krylov layer through fde_pcg /
+fde_gmres: iteration counts within ±1 of the oracle's and final solutions
+within 1e-9 (relative, BASELINE north_star), on the BASELINE configs (the
+2D variable case also at full size via the true-residual property) and on
+the paper's own Example 1 time loop (Table 1)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from test_gpu_ops import oracle_system, oracle_weights, relerr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def gpu_solve(torch, p, solver, restart=30, left=False, maxit=None, rtol=None):
+    from paper_1912_13304_b200 import fde
+    h = fde.Fde.from_problem(p)
+    b = torch.from_numpy(p.rhs.copy()).cuda()
+    x = torch.zeros_like(b)
+    maxit = maxit or p.maxit
+    rtol = rtol or p.rtol
+    if solver == "pcg":
+        st, stats = h.pcg(b, x, rtol, maxit)
+    else:
+        st, stats = h.gmres(b, x, rtol, restart, maxit, left)
+    torch.cuda.synchronize()
+    out = x.cpu().numpy()
+    launches = h.kernel_launches()
+    h.close()
+    return st, stats, out, launches
+
+
+def oracle_solve(p, s, solver, restart=30, left=False, maxit=None, rtol=None):
+    cx, cy = oracle_weights(p, s)
+    Pinv = lambda v: s.prec_solve(v, p.prec, cx, cy)
+    res = []
+    for b in range(p.batch):
+        if solver == "pcg":
+            res.append(O.pcg(s.matvec, Pinv, p.rhs[b], rtol or p.rtol, maxit or p.maxit))
+        else:
+            res.append(O.gmres(s.matvec, Pinv, p.rhs[b], rtol or p.rtol, restart, maxit or p.maxit, left=left))
+    return res
+
+
+SOLVES = [
+    (1, None, 1, "pcg", W.PREC_TAU), (1, None, 3, "pcg", W.PREC_TAU), (1, None, 1, "pcg", W.PREC_NONE),
+    (1, None, 2, "gmres", W.PREC_TAU),
+    (2, None, 1, "gmres", W.PREC_TAU_D), (2, 255, 2, "gmres", W.PREC_TAU), (2, 1023, 1, "gmres", W.PREC_TAU_DSYM),
+    (3, 63, 2, "pcg", W.PREC_TAU), (3, None, 1, "pcg", W.PREC_TAU),
+    (4, 63, 1, "gmres", W.PREC_TAU), (4, 127, 2, "gmres", W.PREC_TAU_D), (4, 255, 1, "gmres", W.PREC_TAU),
+    (5, 255, 4, "pcg", W.PREC_TAU),
+]
+
+
+@pytest.mark.parametrize("cfg,n,batch,solver,prec", SOLVES, ids=lambda v: str(v))
+def test_solver_parity(torch_cuda, cfg, n, batch, solver, prec):
+    p = W.config(cfg, n=n, batch=batch, prec=prec)
+    s = oracle_system(p)
+    st, stats, x, launches = gpu_solve(torch_cuda, p, solver)
+    ref = oracle_solve(p, s, solver)
+    assert launches > 0
+    for b in range(batch):
+        xo, it_o, conv_o, _ = ref[b]
+        assert stats[b]["converged"] == conv_o
+        assert abs(stats[b]["iters"] - it_o) <= 1, (b, stats[b]["iters"], it_o)
+        assert relerr(x[b], xo) <= 1e-9, relerr(x[b], xo)
+        r = p.rhs[b] - s.matvec(x[b])
+        assert np.linalg.norm(r) / np.linalg.norm(p.rhs[b]) <= 1e-9
+
+
+def test_gmres_left_unrestarted_matches_oracle(torch_cuda):
+    p = W.config(2, n=255, prec=W.PREC_TAU_D)
+    s = oracle_system(p)
+    st, stats, x, _ = gpu_solve(torch_cuda, p, "gmres", restart=64, left=True, maxit=64, rtol=1e-7)
+    (xo, it_o, conv_o, _), = oracle_solve(p, s, "gmres", restart=64, left=True, maxit=64, rtol=1e-7)
+    assert abs(stats[0]["iters"] - it_o) <= 1
+    assert relerr(x[0], xo) <= 1e-6
+
+
+def test_cfg4_full_size_residual(torch_cuda):
+    """BASELINE config 4 at n = 1023 (the bench workload): the oracle cannot run
+    466 dense iterations, so check the property that holds at any size — the
+    true residual of the GPU solution, computed by the oracle's dense matvec."""
+    p = W.config(4)
+    s = oracle_system(p)
+    st, stats, x, _ = gpu_solve(torch_cuda, p, "gmres")
+    assert stats[0]["converged"]
+    r = p.rhs[0] - s.matvec(x[0])
+    assert np.linalg.norm(r) / np.linalg.norm(p.rhs[0]) <= 2e-10
+    assert 300 < stats[0]["iters"] < 700   # SURVEY App. A forecast: 466
+
+
+def test_paper_table1_iterations_on_gpu(torch_cuda):
+    """Example 1 time loop with every GMRES solve on the GPU
+    (left, unrestarted, tol 1e-7, P_F = τ·D): the average iteration counts of
+    Table 1 at n1+1 = 64."""
+    from paper_1912_13304_b200 import fde
+    import torch
+    for alpha, printed in ((1.2, 7.2), (1.5, 6.7), (1.8, 6.1)):
+        n = 63
+        ex = W.example1(alpha, n)
+        h = fde.Fde(n, 1, alpha, nu=ex["nu"], dp_field=ex["dp"], dm_field=ex["dm"], prec=W.PREC_TAU_D)
+        u = ex["u0"].copy()
+        its = 0
+        for m in range(1, ex["M"] + 1):
+            b = (ex["nu"] * u + ex["h"] ** alpha * ex["f"](m * ex["ht"]))[None, :]
+            x = np.zeros_like(b)
+            st, stats = h.gmres(np.ascontiguousarray(b), x, 1e-7, 63, 63, left=True)
+            its += stats[0]["iters"]
+            u = x[0]
+        h.close()
+        assert abs(its / ex["M"] - printed) <= 0.15, (alpha, its / ex["M"])

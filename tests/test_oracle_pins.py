@@ -364,3 +364,19 @@ def test_table3_table4_iterations(row):
     ex = W.example2(alpha, beta, n)
     assert abs(O.example2_run(ex, alpha, beta, n, O.PREC_TAU_D) - row[5]) <= 0.25
     assert abs(O.example2_run(ex, alpha, beta, n, O.PREC_NONE) - row[3]) <= 1.5
+
+
+def test_matvec_entries_and_sine_modes():
+    # the one-by-one entry evaluator equals the full product; sine modes are
+    # eigenvectors of τ — the large-size GPU checks rely on both
+    s = _sys2d(n=9)
+    x = np.random.default_rng(4).standard_normal(s.N)
+    idx = [0, 5, 17, 40, 80]
+    assert np.allclose(s.matvec_entries(x, idx), s.matvec(x)[idx], atol=1e-13)
+    s1 = O.System(1, 12, 1.4, 0, 0.2, 1.0, 2.0)
+    x1 = np.random.default_rng(5).standard_normal(12)
+    assert np.allclose(s1.matvec_entries(x1, [0, 3, 11]), s1.matvec(x1)[[0, 3, 11]], atol=1e-13)
+    md = O.sine_mode(9, 3, 7)
+    F = s.symbol_samples(0.7, 1.1)
+    assert np.allclose(s.prec_solve(md, O.PREC_TAU, 0.7, 1.1), md / F[6, 2], atol=1e-14)
+    assert np.allclose(O.sine_mode(12, 5), O.sine_matrix(12)[:, 4])
