@@ -132,6 +132,19 @@ const char* fde_last_error(fde_handle h);
  * (CUDA-graph replays count every node): evidence for the bench. */
 int64_t fde_kernel_launches(fde_handle h);
 
+/* Measurement support (bench.py's roofline leg). Runs `reps`
+ * units W = fde_matvec(x -> y) + fde_tau_apply(x -> z) on the handle's stream
+ * with every kernel launch preceded by a cudaMemsetAsync of `flush`
+ * (flush_bytes > L2 size flushes L2; flush may be NULL with flush_bytes 0)
+ * and bracketed by CUDA events. On return *count is the number of kernels per
+ * unit, us[i] the mean device time (µs) of the i-th kernel of the unit over the
+ * reps and names[i] its static name (library-owned string), for
+ * i < min(*count, max_kernels). x, y, z, flush: device pointers; x must not
+ * alias y or z. Synchronises the stream. */
+fde_status fde_profile_unit(fde_handle h, const double* x, double* y, double* z, int32_t reps, void* flush,
+                            int64_t flush_bytes, int32_t max_kernels, int32_t* count, double* us,
+                            const char** names);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,11 @@ using namespace fde;
 
 namespace {
 
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+
 struct FdeFail {
   fde_status s;
   std::string msg;
@@ -182,6 +187,11 @@ struct fde_handle_s {
   int g_maxit = -1;
 
   std::vector<void*> allocs;
+  // profiling (fde_profile_unit)
+  bool prof = false;
+  void* flush = nullptr;
+  size_t flush_bytes = 0;
+  std::vector<ProfRec> recs;
 
   template <class T>
   T* dalloc(size_t count) {
@@ -210,6 +220,27 @@ LineArgs base_args(fde_handle h) {
   return a;
 }
 
+// Launch bookkeeping: every kernel launch of the library goes through here.
+// In profiling mode (fde_profile_unit) each launch is preceded by an L2 flush
+// and bracketed by CUDA events on the handle's stream.
+template <class F>
+void launch_named(fde_handle h, const char* name, F&& f) {
+  if (h->prof) {
+    if (h->flush) FDE_CUDA(cudaMemsetAsync(h->flush, h->recs.size() & 0xff, h->flush_bytes, h->st));
+    ProfRec r{name, nullptr, nullptr};
+    FDE_CUDA(cudaEventCreate(&r.a));
+    FDE_CUDA(cudaEventCreate(&r.b));
+    FDE_CUDA(cudaEventRecord(r.a, h->st));
+    f();
+    FDE_CUDA(cudaEventRecord(r.b, h->st));
+    h->recs.push_back(r);
+  } else {
+    f();
+  }
+  FDE_CUDA(cudaGetLastError());
+  h->launches++;
+}
+
 // ------------------------------------------------------ kernel dispatchers
 template <int K, bool COL, bool VAR>
 void launch_toep_k(fde_handle h, const LineArgs& a) {
@@ -217,27 +248,24 @@ void launch_toep_k(fde_handle h, const LineArgs& a) {
   auto kern = k_toeplitz_lines<K, KR, COL, VAR, C::FPC>;
   const int npairs = (a.nlines + 1) / 2;
   const int grid = (npairs + C::FPC - 1) / C::FPC;
-  kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a);
-  FDE_CUDA(cudaGetLastError());
-  h->launches++;
+  launch_named(h, COL ? (VAR ? "toeplitz_cols_var" : "toeplitz_cols") : (VAR ? "toeplitz_rows_var" : "toeplitz_rows"),
+               [&] { kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a); });
 }
 template <int K, bool COL>
 void launch_dst_k(fde_handle h, const LineArgs& a) {
   using C = LaunchCfg<K, COL, 1>;
   auto kern = k_dst_lines<K, KR, COL, C::FPC>;
   const int npairs = (a.nlines + 1) / 2;
-  kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a);
-  FDE_CUDA(cudaGetLastError());
-  h->launches++;
+  launch_named(h, COL ? "dst_cols" : "dst_rows",
+               [&] { kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a); });
 }
 template <int K, bool COL>
 void launch_tau_k(fde_handle h, const LineArgs& a) {
   using C = LaunchCfg<K, COL, 1>;
   auto kern = k_tau_lines<K, KR, COL, C::FPC>;
   const int npairs = (a.nlines + 1) / 2;
-  kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a);
-  FDE_CUDA(cudaGetLastError());
-  h->launches++;
+  launch_named(h, COL ? "tau_cols" : "tau_rows",
+               [&] { kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a); });
 }
 
 #define FDE_SWITCH_K(K, CALL)                                           \
@@ -337,9 +365,7 @@ void op_matvec(fde_handle h, const double* x, double* y, const int* gate) {
 
 void op_copy(fde_handle h, const double* src, double* dst) {
   const long long n = (long long)h->vec_elems();
-  k_copy<<<592, 256, 0, h->st>>>(src, dst, n);
-  FDE_CUDA(cudaGetLastError());
-  h->launches++;
+  launch_named(h, "copy", [&] { k_copy<<<592, 256, 0, h->st>>>(src, dst, n); });
 }
 
 // z = P⁻¹ r (a2)
@@ -971,5 +997,63 @@ const char* fde_status_str(fde_status s) {
 const char* fde_last_error(fde_handle h) { return h ? h->err.c_str() : "NULL handle"; }
 
 int64_t fde_kernel_launches(fde_handle h) { return h ? (int64_t)h->launches : 0; }
+
+fde_status fde_profile_unit(fde_handle h, const double* x, double* y, double* z, int32_t reps, void* flush,
+                            int64_t flush_bytes, int32_t max_kernels, int32_t* count, double* us,
+                            const char** names) {
+  if (!h) return FDE_ERR_INVALID_ARG;
+  if (!x || !y || !z || !count || !us || !names || reps < 1 || max_kernels < 1 || flush_bytes < 0 ||
+      (flush_bytes > 0 && !flush) || (const void*)x == (const void*)y || (const void*)x == (const void*)z ||
+      y == z) {
+    h->err = "fde_profile_unit: bad arguments";
+    return FDE_ERR_INVALID_ARG;
+  }
+  try {
+    if (!is_device_ptr(x) || !is_device_ptr(y) || !is_device_ptr(z) || (flush && !is_device_ptr(flush))) {
+      h->err = "fde_profile_unit needs device pointers";
+      return FDE_ERR_INVALID_ARG;
+    }
+    h->flush = flush;
+    h->flush_bytes = (size_t)flush_bytes;
+    h->recs.clear();
+    h->prof = true;
+    try {
+      for (int r = 0; r < reps; ++r) {
+        op_matvec(h, x, y, nullptr);
+        op_tau(h, x, z, nullptr);
+      }
+    } catch (...) {
+      h->prof = false;
+      throw;
+    }
+    h->prof = false;
+    FDE_CUDA(cudaStreamSynchronize(h->st));
+    const int total = (int)h->recs.size();
+    const int nk = total / reps;
+    *count = nk;
+    for (int i = 0; i < nk && i < max_kernels; ++i) {
+      double acc = 0.0;
+      for (int r = 0; r < reps; ++r) {
+        float ms = 0.f;
+        FDE_CUDA(cudaEventElapsedTime(&ms, h->recs[r * nk + i].a, h->recs[r * nk + i].b));
+        acc += ms;
+      }
+      us[i] = 1e3 * acc / reps;
+      names[i] = h->recs[i].name;
+    }
+    for (auto& r : h->recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    h->recs.clear();
+    return FDE_OK;
+  } catch (const FdeFail& f) {
+    h->prof = false;
+    return fail(h, f);
+  } catch (...) {
+    h->prof = false;
+    return fail(h, FdeFail{FDE_ERR_CUDA, "unexpected exception"});
+  }
+}
 
 }  // extern "C"

@@ -77,6 +77,10 @@ lib.fde_last_error.argtypes = [_H]
 lib.fde_last_error.restype = ctypes.c_char_p
 lib.fde_kernel_launches.argtypes = [_H]
 lib.fde_kernel_launches.restype = ctypes.c_int64
+lib.fde_profile_unit.argtypes = [_H, _P, _P, _P, ctypes.c_int32, _P, ctypes.c_int64, ctypes.c_int32,
+                                 ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double),
+                                 ctypes.POINTER(ctypes.c_char_p)]
+lib.fde_profile_unit.restype = ctypes.c_int
 
 
 def fde_status_str(s: int) -> str:
@@ -171,6 +175,21 @@ class Fde:
 
     def kernel_launches(self) -> int:
         return int(lib.fde_kernel_launches(self._h))
+
+    def profile_unit(self, x, y, z, reps: int = 20, flush=None):
+        """fde_profile_unit: per-kernel mean device µs of one unit
+        (matvec x->y + τ-solve x->z), each launch after an L2 flush of the
+        device buffer `flush` (a uint8 CUDA tensor) if given. Returns
+        [(name, µs), ...] in launch order."""
+        MAXK = 16
+        us = (ctypes.c_double * MAXK)()
+        names = (ctypes.c_char_p * MAXK)()
+        cnt = ctypes.c_int32(0)
+        fp = 0 if flush is None else flush.data_ptr()
+        fb = 0 if flush is None else flush.numel() * flush.element_size()
+        self._check(lib.fde_profile_unit(self._h, _ptr(x), _ptr(y), _ptr(z), reps, fp or None, fb, MAXK,
+                                         ctypes.byref(cnt), us, names))
+        return [(names[i].decode(), us[i]) for i in range(min(cnt.value, MAXK))]
 
     def close(self):
         if self._h:
