@@ -21,19 +21,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force: bool = False, log: str = None) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, log: str = None, out: str = None, extra=()) -> str:
+    """Compile libfde.so (or `out` with extra nvcc flags, for A/B variants)."""
+    if out is None and not force and up_to_date():
         return OUT
+    out = out or OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc] + NVCC_FLAGS + ["-o", OUT, SRC]
+    cmd = [nvcc] + NVCC_FLAGS + list(extra) + ["-o", out, SRC]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if log:
         with open(log, "w") as f:
             f.write(r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(r.stderr[-4000:])
-        raise RuntimeError("nvcc failed building libfde.so")
-    return OUT
+        raise RuntimeError("nvcc failed building %s" % out)
+    return out
 
 
 if __name__ == "__main__":

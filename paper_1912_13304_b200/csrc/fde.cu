@@ -44,7 +44,10 @@ struct FdeFail {
                     std::string(#call) + ": " + cudaGetErrorString(e_)};                \
   } while (0)
 
-constexpr int KMIN = 6, KMAX = 13, KR = 4;
+#ifndef FDE_KR
+#define FDE_KR 4
+#endif
+constexpr int KMIN = 6, KMAX = 13, KR = FDE_KR;  // log2 points per thread in the FFT engine
 
 // ------------------------------------------------------------------ host maths
 std::vector<double> grunwald(double alpha, int K) {  // g_k = (-1)^k C(α,k)
@@ -137,14 +140,16 @@ struct LaunchCfg {
   using G = FftGeom<K, KR>;
   static constexpr int SPG = G::SM_STRIDE * 16 * NBUF;      // smem bytes per FFT group
   static constexpr int SMEM_CAP = 200 * 1024;
-  static constexpr int MAXT = NBUF == 2 ? 256 : 512;        // threads per CTA (register budget)
-  static constexpr int BY_SMEM = SMEM_CAP / SPG > 0 ? SMEM_CAP / SPG : 1;
-  static constexpr int BY_THR = MAXT / G::P > 0 ? MAXT / G::P : 1;
-  static constexpr int WANT = COL ? 8 : (256 / G::P > 0 ? 256 / G::P : 1);
+  static constexpr int BY_SMEM = (SMEM_CAP - TW_SMEM_QUARTER * (G::L / 4) * 16) / SPG > 0 ? (SMEM_CAP - TW_SMEM_QUARTER * (G::L / 4) * 16) / SPG : 1;
+  static constexpr int BY_THR = 512 / G::P > 0 ? 512 / G::P : 1;  // <= 512 threads: 128 registers/thread
+  // rows: ~128 threads per CTA (one line pair at n = 1023), so that every pair of
+  // a pass is resident at once; columns: >= 2 adjacent pairs (4 columns = one
+  // 32-byte sector per row) per CTA
+  static constexpr int WANT = COL ? (128 / G::P > 2 ? 128 / G::P : 2) : (128 / G::P > 1 ? 128 / G::P : 1);
   static constexpr int FPC = WANT < BY_SMEM ? (WANT < BY_THR ? WANT : BY_THR) : (BY_SMEM < BY_THR ? BY_SMEM : BY_THR);
   static constexpr int THREADS = FPC * G::P;
-  static constexpr int SMEM = FPC * SPG;
-  static constexpr bool FITS = SPG <= 227 * 1024;
+  static constexpr int SMEM = FPC * SPG + TW_SMEM_QUARTER * (G::L / 4) * 16;   // + the quarter twiddle table
+  static constexpr bool FITS = SPG + TW_SMEM_QUARTER * (G::L / 4) * 16 <= 227 * 1024;
 };
 
 }  // namespace
@@ -160,6 +165,7 @@ struct fde_handle_s {
 
   // tables
   double2* tw = nullptr;
+  double2* twp = nullptr;
   double2 *mu_x = nullptr, *mu_y = nullptr;
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
   double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
@@ -217,6 +223,7 @@ LineArgs base_args(fde_handle h) {
   a.n = h->n;
   a.N = h->N;
   a.tw = h->tw;
+  a.twp = h->twp;
   return a;
 }
 
@@ -316,6 +323,7 @@ void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const dou
   const bool var = col ? h->var_y : h->var_x;
   if (!var) {
     a.mu = col ? h->mu_y : h->mu_x;
+    a.nu = 0.0;  // ν is folded into μ_x (ν + λ: νI added to the circulant), see build()
     if (col) { FDE_SWITCH_K(h->K, (launch_toep_k<KK, true, false>(h, a))); }
     else { FDE_SWITCH_K(h->K, (launch_toep_k<KK, false, false>(h, a))); }
     return;
@@ -447,10 +455,27 @@ void build(fde_handle h, const fde_desc* d) {
   h->var_y = two && (d->ep_field || d->em_field);
   const double ywt = d->ywt > 0.0 ? d->ywt : 1.0;
 
-  // twiddles
-  std::vector<double2> tw(L / 2);
-  for (int e = 0; e < L / 2; ++e) { auto z = root_of_unity(e, L); tw[e] = make_double2(z.real(), z.imag()); }
+  // twiddles: quarter table exp(-2πi r/L), r < L/4 (fft_engine.cuh tw_lookup)
+  std::vector<double2> tw(L / 4);
+  for (int e = 0; e < L / 4; ++e) { auto z = root_of_unity(e, L); tw[e] = make_double2(z.real(), z.imag()); }
   h->tw = h->upload(tw);
+  {  // per-pass twiddle tables (FDE_TW_MODE 1): [pass I][q][t_lo] = W_L^{(t_lo << (K-lo-ka)) bitrev_ka(q)}
+    const int K = h->K, k = KR;
+    std::vector<double2> tp;
+    for (int I = 0; (I * k) < K; ++I) {
+      const int lo = K - (I + 1) * k > 0 ? K - (I + 1) * k : 0;
+      const int ka = K - I * k - lo;
+      if (lo == 0) break;
+      for (int q = 0; q < (1 << k); ++q)
+        for (int tl = 0; tl < (1 << lo); ++tl) {
+          const long long e = q < (1 << ka) ? ((long long)tl << (K - lo - ka)) * bitrev_host(q, ka) : 0;
+          auto z = root_of_unity(e, L);
+          tp.push_back(make_double2(z.real(), z.imag()));
+        }
+    }
+    if (tp.empty()) tp.push_back(make_double2(1.0, 0.0));
+    h->twp = h->upload(tp);
+  }
 
   // circulant eigenvalues λ = DFT_L(c), c = first column of the embedding
   auto lambda = [&](double order) {
@@ -461,7 +486,7 @@ void build(fde_handle h, const fde_desc* d) {
     host_fft(c);
     return c;
   };
-  auto make_dir = [&](double order, bool var, double cpl, double cmi, double wgt, double2*& mu, double*& lS,
+  auto make_dir = [&](double order, bool var, double cpl, double cmi, double wgt, double shift, double2*& mu, double*& lS,
                       double*& lK, double*& cPf, double*& cMf, const std::vector<double>& fp,
                       const std::vector<double>& fm) {
     std::vector<std::complex<double>> lam = lambda(order);
@@ -471,7 +496,8 @@ void build(fde_handle h, const fde_desc* d) {
       std::vector<double2> mv(L);
       for (int s = 0; s < L; ++s) {
         const std::complex<double> l = lam[bitrev_host(s, h->K)];
-        mv[s] = make_double2(wgt * (cpl + cmi) * l.real() * invL, wgt * (cpl - cmi) * l.imag() * invL);
+        // C(ν + λ) restricted to the leading n×n block is νI + (the Toeplitz part)
+        mv[s] = make_double2((shift + wgt * (cpl + cmi) * l.real()) * invL, wgt * (cpl - cmi) * l.imag() * invL);
       }
       mu = h->upload(mv);
     } else {
@@ -493,8 +519,8 @@ void build(fde_handle h, const fde_desc* d) {
       cMf = h->upload(q);
     }
   };
-  make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, h->mu_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm);
-  if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, h->mu_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em);
+  make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, d->nu, h->mu_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm);
+  if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, 0.0, h->mu_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em);
 
   // preconditioner tables
   const int prec = d->prec;
@@ -650,6 +676,7 @@ __global__ void k_reset_counters(Counters* c, SolveState* s, int batch) {
   if (threadIdx.x == 0) {
     c->active = batch;
     c->unfinished = batch;
+    c->loops = 0;
     for (int i = 0; i < 64; ++i) c->tickets[i] = 0u;
   }
   if ((int)threadIdx.x < batch) {
@@ -682,6 +709,57 @@ void ensure_krylov(fde_handle h, int nvecV) {
 
 #define VGRID dim3(RED_BLOCKS, h->batch)
 
+// Build `*out` = [WHILE(cond) { body() ; k_loop_ctrl }] by capturing body()
+// into the conditional node's body graph. Returns the kernel nodes per body.
+template <class F>
+int build_while_graph(fde_handle h, cudaGraphExec_t* out, int maxloops, F&& body) {
+  cudaGraph_t g;
+  FDE_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle ch;
+  FDE_CUDA(cudaGraphConditionalHandleCreate(&ch, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = ch;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cn;
+  FDE_CUDA(cudaGraphAddNode(&cn, g, nullptr, 0, &cp));
+  cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+  cudaStream_t cs;
+  FDE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaStream_t saved = h->st;
+  const long long l0 = h->launches;
+  h->st = cs;
+  try {
+    FDE_CUDA(cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    body();
+    k_loop_ctrl<<<1, 1, 0, cs>>>(ch, h->ctr, maxloops);
+    FDE_CUDA(cudaGetLastError());
+    cudaGraph_t captured;
+    FDE_CUDA(cudaStreamEndCapture(cs, &captured));
+  } catch (...) {
+    h->st = saved;
+    cudaGraph_t junk;
+    cudaStreamEndCapture(cs, &junk);
+    cudaStreamDestroy(cs);
+    cudaGraphDestroy(g);
+    throw;
+  }
+  const int nodes = (int)(h->launches - l0) + 1;
+  h->launches = l0;
+  h->st = saved;
+  cudaStreamDestroy(cs);
+  FDE_CUDA(cudaGraphInstantiate(out, g, 0));
+  cudaGraphDestroy(g);
+  return nodes;
+}
+
+int read_loops(fde_handle h) {
+  int loops = 0;
+  FDE_CUDA(cudaMemcpy(&loops, &h->ctr->loops, sizeof(int), cudaMemcpyDeviceToHost));
+  return loops;
+}
+
 // one PCG iteration (device-gated)
 void pcg_iteration(fde_handle h, const VecArgs& va) {
   const int* gate = &h->ctr->active;
@@ -708,46 +786,23 @@ fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int ma
   h->launches++;
   FDE_CUDA(cudaGetLastError());
 
-  // a chunk of iterations captured once as a CUDA graph
-  const int chunk = 8;
+  // the whole iteration loop is ONE graph launch: a conditional WHILE node
+  // whose body is one PCG iteration plus k_loop_ctrl (no host round trips)
   if (!h->g_pcg || h->g_rtol != rtol || h->g_maxit != maxit) {
     if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
-    cudaStream_t cs;
-    FDE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    cudaStream_t saved = h->st;
-    h->st = cs;
-    const long long l0 = h->launches;
-    cudaGraph_t g;
-    FDE_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < chunk; ++i) pcg_iteration(h, va);
-    FDE_CUDA(cudaStreamEndCapture(cs, &g));
-    FDE_CUDA(cudaGraphInstantiate(&h->g_pcg, g, 0));
-    cudaGraphDestroy(g);
-    h->g_pcg_nodes = (int)(h->launches - l0);
-    h->launches = l0;
-    h->st = saved;
-    cudaStreamDestroy(cs);
+    h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { pcg_iteration(h, va); });
     h->g_rtol = rtol;
     h->g_maxit = maxit;
   }
-  int flag = 1;
-  int* hflag = nullptr;
-  FDE_CUDA(cudaMallocHost(&hflag, sizeof(int)));
-  for (int done = 0; done < maxit; done += chunk) {
-    FDE_CUDA(cudaGraphLaunch(h->g_pcg, h->st));
-    h->launches += h->g_pcg_nodes;
-    FDE_CUDA(cudaMemcpyAsync(hflag, &h->ctr->active, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    FDE_CUDA(cudaStreamSynchronize(h->st));
-    flag = *hflag;
-    if (flag == 0) break;
-  }
-  cudaFreeHost(hflag);
+  FDE_CUDA(cudaGraphLaunch(h->g_pcg, h->st));
   if (is_device_ptr(x)) {
     FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
   } else {
     FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   }
-  return worst_status(h, st, true);
+  const fde_status ws = worst_status(h, st, true);
+  h->launches += (long long)read_loops(h) * h->g_pcg_nodes;
+  return ws;
 }
 
 // ---------------------------------------------------------------- GMRES
@@ -819,45 +874,25 @@ fde_status run_gmres(fde_handle h, const double* b, double* x, double rtol, int 
   h->launches++;
   FDE_CUDA(cudaGetLastError());
 
+  // one graph launch per solve: WHILE(some RHS unfinished) { one restart cycle }
+  const int max_cycles = maxit / restart + 2;
   if (!h->g_gm || h->g_gm_restart != restart || h->g_gm_left != left || h->g_rtol != rtol || h->g_maxit != maxit) {
     if (h->g_gm) { cudaGraphExecDestroy(h->g_gm); h->g_gm = nullptr; }
-    cudaStream_t cs;
-    FDE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    cudaStream_t saved = h->st;
-    h->st = cs;
-    const long long l0 = h->launches;
-    cudaGraph_t g;
-    FDE_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    gmres_cycle(h, va, restart, left);
-    FDE_CUDA(cudaStreamEndCapture(cs, &g));
-    FDE_CUDA(cudaGraphInstantiate(&h->g_gm, g, 0));
-    cudaGraphDestroy(g);
-    h->g_gm_nodes = (int)(h->launches - l0);
-    h->launches = l0;
-    h->st = saved;
-    cudaStreamDestroy(cs);
+    h->g_gm_nodes = build_while_graph(h, &h->g_gm, max_cycles, [&] { gmres_cycle(h, va, restart, left); });
     h->g_gm_restart = restart;
     h->g_gm_left = left;
     h->g_rtol = rtol;
     h->g_maxit = maxit;
   }
-  int* hflag = nullptr;
-  FDE_CUDA(cudaMallocHost(&hflag, sizeof(int)));
-  const int max_cycles = maxit / restart + 2;
-  for (int c = 0; c < max_cycles; ++c) {
-    FDE_CUDA(cudaGraphLaunch(h->g_gm, h->st));
-    h->launches += h->g_gm_nodes;
-    FDE_CUDA(cudaMemcpyAsync(hflag, &h->ctr->unfinished, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    FDE_CUDA(cudaStreamSynchronize(h->st));
-    if (*hflag == 0) break;
-  }
-  cudaFreeHost(hflag);
+  FDE_CUDA(cudaGraphLaunch(h->g_gm, h->st));
   if (is_device_ptr(x)) {
     FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
   } else {
     FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   }
-  return worst_status(h, st, false);
+  const fde_status ws = worst_status(h, st, false);
+  h->launches += (long long)read_loops(h) * h->g_gm_nodes;
+  return ws;
 }
 
 void free_handle(fde_handle h) {

@@ -126,30 +126,85 @@ __device__ __forceinline__ void dft_dit(double2 (&v)[1 << k]) {
   }
 }
 
-// multiply v[q] by w^{bitrev_ka(q)} for the active-q range (q < 2^ka); w = base twiddle.
-template <int k, int ka>
-__device__ __forceinline__ void apply_twiddles(double2 (&v)[1 << k], double2 w) {
-  constexpr int RA = 1 << ka;
-  double2 pw[RA];
-  pw[0] = make_double2(1.0, 0.0);
-  pw[1] = w;
-#pragma unroll
-  for (int r = 2; r < RA; ++r) pw[r] = c_mul(pw[r >> 1], pw[r - (r >> 1)]);
-#pragma unroll
-  for (int q = 1; q < RA; ++q) v[q] = c_mul(v[q], pw[bitrev_c(q, ka)]);
+// v[q] *= W_L^{SIGMA * base_e * bitrev_ka(q)} for q < 2^ka, with the roots read
+// from a shared-memory quarter table tw[r] = exp(-2 pi i r / L), r < L/4
+// (staged once per CTA by load_twiddles): W^{r + c L/4} = W^r (-i)^c, the
+// quarter turn is a swap plus sign flips (integer ops on the ALU pipe), and
+// conjugation for SIGMA = +1 is folded into the product. base_e * bitrev(q) < L.
+__device__ __forceinline__ double2 tw_lookup(const double2* tw, int e, int L) {
+  const int quarter = L >> 2;
+  const double2 w = tw[e & (quarter - 1)];
+  const int c = e / quarter;  // 0..3 (power of two: a shift)
+  const long long SGN = (long long)0x8000000000000000ULL;
+  const long long xb = __double_as_longlong(w.x), yb = __double_as_longlong(w.y);
+  // (x + iy)(-i) = y - ix
+  long long rx = (c & 1) ? yb : xb;
+  long long ry = (c & 1) ? (xb ^ SGN) : yb;
+  const long long s2 = (c & 2) ? SGN : 0LL;
+  return make_double2(__longlong_as_double(rx ^ s2), __longlong_as_double(ry ^ s2));
 }
 
-template <class G, int I, int SIGMA>
-__device__ __forceinline__ double2 base_twiddle(int t, const double2* __restrict__ tw) {
+// stage the quarter twiddle table into shared memory (all threads of the CTA;
+// the caller's next __syncthreads publishes it)
+__device__ __forceinline__ void load_twiddles(double2* sm_tw, const double2* __restrict__ tw_glob, int L) {
+  for (int i = threadIdx.x; i < (L >> 2); i += blockDim.x) sm_tw[i] = __ldg(&tw_glob[i]);
+}
+
+template <int SIGMA>
+__device__ __forceinline__ double2 c_mul_tw(double2 a, double2 w) {  // a * (SIGMA<0 ? w : conj w)
+  if (SIGMA < 0) return c_mul(a, w);
+  return make_double2(fma(a.x, w.x, a.y * w.y), fma(a.y, w.x, -a.x * w.y));
+}
+template <int k, int ka, int SIGMA>
+__device__ __forceinline__ void apply_twiddles(double2 (&v)[1 << k], int base_e, int L, const double2* tw) {
+  constexpr int RA = 1 << ka;
+#pragma unroll
+  for (int q = 1; q < RA; ++q) v[q] = c_mul_tw<SIGMA>(v[q], tw_lookup(tw, base_e * bitrev_c(q, ka), L));
+}
+
+template <class G, int I>
+__device__ __forceinline__ int base_exponent(int t) {
   constexpr int l = G::lo(I), a = G::ka(I);
-  const int tlo = t & ((1 << l) - 1);
-  const double2 w = __ldg(&tw[tlo << (G::K - l - a)]);
-  return SIGMA < 0 ? w : c_conj(w);
+  return (t & ((1 << l) - 1)) << (G::K - l - a);
+}
+
+// Twiddle sources. FDE_TW_MODE 0: the shared-memory quarter table (tw_lookup);
+// 1: exact per-pass tables in global memory, entry [pass I][q][t_lo] =
+// W_L^{(t_lo << (K-lo-ka)) * bitrev_ka(q)} (no index arithmetic, no sign
+// logic; consecutive threads read consecutive entries), read through L1.
+#ifndef FDE_TW_MODE
+#define FDE_TW_MODE 1
+#endif
+constexpr int TW_SMEM_QUARTER = FDE_TW_MODE == 0 ? 1 : 0;  // smem holds the quarter table
+struct TwSrc {
+  const double2* sm;   // quarter table in shared memory (mode 0)
+  const double2* gp;   // per-pass tables in global memory (mode 1)
+};
+template <int K, int k>
+__host__ __device__ constexpr int tw_pass_offset(int I) {
+  int o = 0;
+  for (int i = 0; i < I; ++i) {
+    const int lo = K - (i + 1) * k > 0 ? K - (i + 1) * k : 0;
+    if (lo > 0) o += (1 << k) << lo;
+  }
+  return o;
+}
+template <class G, int I, int SIGMA>
+__device__ __forceinline__ void pass_twiddles(double2 (&v)[G::R], int t, const TwSrc& tw) {
+  constexpr int l = G::lo(I), a = G::ka(I);
+  if (l == 0) return;
+#if FDE_TW_MODE == 0
+  apply_twiddles<G::k, a, SIGMA>(v, base_exponent<G, I>(t), G::L, tw.sm);
+#else
+  const double2* tp = tw.gp + tw_pass_offset<G::K, G::k>(I) + (t & ((1 << l) - 1));
+#pragma unroll
+  for (int q = 1; q < (1 << a); ++q) v[q] = c_mul_tw<SIGMA>(v[q], tp[q << l]);  // plain load: stays below the barrier
+#endif
 }
 
 // DIF pass I on registers (no memory traffic).
 template <class G, int I, int SIGMA, bool HALF_ZERO>
-__device__ __forceinline__ void dif_pass(double2 (&v)[G::R], int t, const double2* __restrict__ tw) {
+__device__ __forceinline__ void dif_pass(double2 (&v)[G::R], int t, const TwSrc& tw) {
   constexpr int a = G::ka(I);
   if (HALF_ZERO && a == G::k) {
     // upper half of the inputs are zero: first radix-2 stage is a copy/twiddle
@@ -171,13 +226,13 @@ __device__ __forceinline__ void dif_pass(double2 (&v)[G::R], int t, const double
   } else {
     dft_dif<G::k, a, SIGMA>(v);
   }
-  if (G::lo(I) > 0) apply_twiddles<G::k, a>(v, base_twiddle<G, I, SIGMA>(t, tw));
+  pass_twiddles<G, I, SIGMA>(v, t, tw);
 }
 
 template <class G, int I, int SIGMA>
-__device__ __forceinline__ void dit_pass(double2 (&v)[G::R], int t, const double2* __restrict__ tw) {
+__device__ __forceinline__ void dit_pass(double2 (&v)[G::R], int t, const TwSrc& tw) {
   constexpr int a = G::ka(I);
-  if (G::lo(I) > 0) apply_twiddles<G::k, a>(v, base_twiddle<G, I, SIGMA>(t, tw));
+  pass_twiddles<G, I, SIGMA>(v, t, tw);
   dft_dit<G::k, a, SIGMA>(v);
 }
 
@@ -195,7 +250,7 @@ __device__ __forceinline__ void sm_load(const double2* sm, double2 (&v)[G::R], i
 // Helper to unroll passes with compile-time indices.
 template <class G, int I, int SIGMA, bool HALF_ZERO>
 struct DifChain {
-  __device__ __forceinline__ static void run(double2 (&v)[G::R], double2* sm, int t, const double2* __restrict__ tw) {
+  __device__ __forceinline__ static void run(double2 (&v)[G::R], double2* sm, int t, const TwSrc& tw) {
     if (I > 0) {
       sm_store<G>(sm, v, t, I - 1);
       __syncthreads();
@@ -207,12 +262,12 @@ struct DifChain {
 };
 template <class G, int SIGMA, bool HALF_ZERO>
 struct DifChain<G, G::NP, SIGMA, HALF_ZERO> {
-  __device__ __forceinline__ static void run(double2 (&)[G::R], double2*, int, const double2* __restrict__) {}
+  __device__ __forceinline__ static void run(double2 (&)[G::R], double2*, int, const TwSrc&) {}
 };
 
 template <class G, int I, int SIGMA>
 struct DitChain {  // runs passes I, I-1, ..., 0
-  __device__ __forceinline__ static void run(double2 (&v)[G::R], double2* sm, int t, const double2* __restrict__ tw) {
+  __device__ __forceinline__ static void run(double2 (&v)[G::R], double2* sm, int t, const TwSrc& tw) {
     if (I < G::NP - 1) {
       sm_store<G>(sm, v, t, I + 1);
       __syncthreads();
@@ -224,7 +279,7 @@ struct DitChain {  // runs passes I, I-1, ..., 0
 };
 template <class G, int SIGMA>
 struct DitChain<G, -1, SIGMA> {
-  __device__ __forceinline__ static void run(double2 (&)[G::R], double2*, int, const double2* __restrict__) {}
+  __device__ __forceinline__ static void run(double2 (&)[G::R], double2*, int, const TwSrc&) {}
 };
 
 // Full chains. v enters holding pass-0 inputs (DIF) / pass-(NP-1) inputs (DIT)
@@ -232,11 +287,11 @@ struct DitChain<G, -1, SIGMA> {
 // frequency order) / pass-0 outputs (DIT; positions (q<<(K-k))|t, natural order).
 // Every thread of the CTA must call these (they contain __syncthreads).
 template <class G, int SIGMA, bool HALF_ZERO>
-__device__ __forceinline__ void dif_chain(double2 (&v)[G::R], double2* sm, int t, const double2* __restrict__ tw) {
+__device__ __forceinline__ void dif_chain(double2 (&v)[G::R], double2* sm, int t, const TwSrc& tw) {
   DifChain<G, 0, SIGMA, HALF_ZERO>::run(v, sm, t, tw);
 }
 template <class G, int SIGMA>
-__device__ __forceinline__ void dit_chain(double2 (&v)[G::R], double2* sm, int t, const double2* __restrict__ tw) {
+__device__ __forceinline__ void dit_chain(double2 (&v)[G::R], double2* sm, int t, const TwSrc& tw) {
   DitChain<G, G::NP - 1, SIGMA>::run(v, sm, t, tw);
 }
 

@@ -14,7 +14,7 @@
 
 namespace fde {
 
-constexpr int RED_BLOCKS = 296;   // 2 x 148 SMs
+constexpr int RED_BLOCKS = 592;   // 4 x 148 SMs: enough loads in flight for HBM/L2 rate
 constexpr int RED_THREADS = 256;
 constexpr int MAX_RESTART = 64;
 
@@ -47,6 +47,8 @@ struct GmresSmall {          // one per RHS
 struct Counters {            // device counters
   int active;                // # RHS with cyc_active (gates Arnoldi/PCG kernels)
   int unfinished;            // # RHS not finished (gates end-of-cycle kernels)
+  int loops;                 // while-loop bodies executed (launch accounting)
+  int pad;
   unsigned tickets[64];      // per-RHS last-block tickets (batch <= 8, 8 slots each)
 };
 
@@ -98,6 +100,7 @@ __device__ __forceinline__ void finalize(const double* part, int nvec, double* o
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = wid; i < nvec; i += nw) {
     double s = 0.0;
+#pragma unroll 8
     for (int bx = lane; bx < RED_BLOCKS; bx += 32) s += __ldcg(part + (size_t)i * RED_BLOCKS + bx);
     s = warp_sum(s);
     if (lane == 0) out[i] = s;
@@ -118,7 +121,7 @@ struct VecArgs {
   int left;
 };
 
-#define FDE_GRID_LOOP(e) for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x)
+#define FDE_GRID_LOOP(e) _Pragma("unroll 4") for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x)
 
 __device__ __forceinline__ void mark_finished(VecArgs& a, SolveState& s) {
   if (s.cyc_active) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
@@ -127,7 +130,7 @@ __device__ __forceinline__ void mark_finished(VecArgs& a, SolveState& s) {
 
 // ============================================================ PCG (a3) ====
 // init: x = 0, r = b; ‖b‖
-__global__ void k_pcg_init(VecArgs a, const double* __restrict__ b, double* x, double* r) {
+__global__ void k_pcg_init(VecArgs a, const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r) {
   const int rb = blockIdx.y, N = a.N;
   const size_t o = (size_t)rb * N;
   double acc[1] = {0.0};
@@ -163,7 +166,7 @@ __global__ void k_pcg_init(VecArgs a, const double* __restrict__ b, double* x, d
 }
 
 // p = z; rho = r·z
-__global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const double* __restrict__ z, double* p) {
+__global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const double* __restrict__ z, double* __restrict__ p) {
   const int rb = blockIdx.y, N = a.N;
   const size_t o = (size_t)rb * N;
   double acc[1] = {0.0};
@@ -219,7 +222,8 @@ __global__ void k_pcg_pq(VecArgs a, const double* __restrict__ p, const double* 
 }
 
 // x += α p ; r -= α q ; ‖r‖ ; convergence (‖r‖ <= rtol ‖b‖, R10)
-__global__ void k_pcg_xr(VecArgs a, const double* __restrict__ p, const double* __restrict__ q, double* x, double* r) {
+__global__ void k_pcg_xr(VecArgs a, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
+                         double* __restrict__ r) {
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -286,7 +290,7 @@ __global__ void k_pcg_rz(VecArgs a, const double* __restrict__ r, const double* 
   }
 }
 
-__global__ void k_pcg_p(VecArgs a, const double* __restrict__ z, double* p) {
+__global__ void k_pcg_p(VecArgs a, const double* __restrict__ z, double* __restrict__ p) {
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -560,6 +564,14 @@ __global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const doub
       }
     }
   }
+}
+
+// while-loop control of a CUDA graph (conditional WHILE node): keep looping
+// while some RHS is still iterating, at most maxloops bodies.
+__global__ void k_loop_ctrl(cudaGraphConditionalHandle hdl, Counters* c, int maxloops) {
+  const int loops = c->loops + 1;
+  c->loops = loops;
+  cudaGraphSetConditional(hdl, (c->active > 0 && loops < maxloops) ? 1u : 0u);
 }
 
 // plain helpers -------------------------------------------------------------

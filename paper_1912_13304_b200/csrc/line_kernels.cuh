@@ -25,7 +25,8 @@ struct LineArgs {
   int nlines;             // number of lines (rows: batch*n_rows, cols: batch*n)
   int N;                  // elements per RHS (n or n*n)
   double nu;              // shift ν·x added to the output (0 to skip)
-  const double2* tw;      // twiddles exp(-2 pi i e/L), e < L/2
+  const double2* tw;      // quarter twiddle table exp(-2 pi i r/L), r < L/4 (FDE_TW_MODE 0)
+  const double2* twp;     // per-pass twiddle tables (FDE_TW_MODE 1, fft_engine.cuh)
   const double2* mu;      // const Toeplitz: complex multiplier, bit-reversed order, 1/L folded
   const double* lamS;     // variable Toeplitz: Re λ / L (bit-reversed order)
   const double* lamK;     // variable Toeplitz: Im λ / L (bit-reversed order)
@@ -42,21 +43,44 @@ struct LineArgs {
 };
 
 // line addressing ----------------------------------------------------------
-template <bool COL>
-struct LineAddr {
-  // element p of line l: rows -> l*n + p ; cols -> b*N + p*n + c with l = b*n + c
-  __device__ __forceinline__ static long long off(int l, int p, int n, int N) {
-    if (!COL) return (long long)l * n + p;
-    const int b = l / n, c = l - b * n;
-    return (long long)b * N + (long long)p * n + c;
-  }
-  // field index (coefficients shared by all RHS)
-  __device__ __forceinline__ static int fidx(int l, int p, int n, int N) {
-    if (!COL) return (int)(((long long)l * n + p) % N);
-    const int c = l % n;
-    return p * n + c;
-  }
+// Element p of line l is at base + p*stride; its coefficient-field index is
+// fbase + p*stride (fields are shared by all RHS).
+//   rows: l = b*rows + r  -> base = l*n, stride 1, fbase = r*n
+//   cols: l = b*n + c     -> base = b*N + c, stride n, fbase = c
+struct Line {
+  long long base;
+  int stride, fbase;
 };
+template <bool COL>
+__device__ __forceinline__ Line line_of(int l, int n, int N) {
+  Line L;
+  if (!COL) {
+    const int rows = N / n;
+    L.base = (long long)l * n;
+    L.stride = 1;
+    L.fbase = (l % rows) * n;
+  } else {
+    const int b = l / n, c = l - b * n;
+    L.base = (long long)b * N + c;
+    L.stride = n;
+    L.fbase = c;
+  }
+  return L;
+}
+
+// 1/x to ~1 ulp for 1e-30 < x < 1e30: fp32 seed + two Newton steps (FP64 FMA),
+// avoiding the IEEE division slow path inside the transform kernels.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r = (double)__frcp_rn((float)x);
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Threads per CTA x resident CTAs per SM = 512: caps registers at 128 so that
+// all line pairs of an n = 1023 pass are resident in one wave.
+__host__ __device__ constexpr int min_blocks_for(int threads) { return threads >= 512 ? 1 : 512 / threads; }
 
 template <class G, bool COL, int FPC>
 struct LineMap {
@@ -72,19 +96,23 @@ struct LineMap {
 // d+ T x + d- Tᵀ x (diagonals multiply after the product).
 // ---------------------------------------------------------------------------
 template <int K, int k, bool COL, bool VAR, int FPC>
-__global__ void __launch_bounds__(FPC * (1 << (K - k)))
+__global__ void __launch_bounds__(FPC * (1 << (K - k)), min_blocks_for(FPC * (1 << (K - k))))
 k_toeplitz_lines(LineArgs a) {
   using G = FftGeom<K, k>;
   using M = LineMap<G, COL, FPC>;
-  extern __shared__ double2 smem[];
+  extern __shared__ double2 smem_all[];
   if (a.gate && *a.gate == 0) return;
+  double2* sm_tw = smem_all;
+  double2* smem = smem_all + TW_SMEM_QUARTER * (G::L >> 2);
+  const TwSrc tws{sm_tw, a.twp};
   const int f = M::group(), t = M::lane();
   double2* sm = smem + (size_t)f * G::SM_STRIDE * (VAR ? 2 : 1);
   double2* smZ = sm + G::SM_STRIDE;
   const int g = blockIdx.x * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
-  const int n = a.n, N = a.N;
+  const int n = a.n;
+  const Line A0 = line_of<COL>(v0 ? l0 : 0, n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, n, a.N);
 
   double2 v[G::R];
 #pragma unroll
@@ -92,29 +120,33 @@ k_toeplitz_lines(LineArgs a) {
     const int p = (q << (K - k)) | t;
     double re = 0.0, im = 0.0;
     if (p < n) {
-      if (v0) re = __ldg(a.x + LineAddr<COL>::off(l0, p, n, N));
-      if (v1) im = __ldg(a.x + LineAddr<COL>::off(l1, p, n, N));
+      if (v0) re = __ldg(a.x + A0.base + (long long)p * A0.stride);
+      if (v1) im = __ldg(a.x + A1.base + (long long)p * A1.stride);
     }
     v[q] = make_double2(re, im);
   }
 #pragma unroll
   for (int q = G::R / 2; q < G::R; ++q) v[q] = make_double2(0.0, 0.0);
+  if (TW_SMEM_QUARTER) {
+    load_twiddles(sm_tw, a.tw, G::L);
+    __syncthreads();
+  }
 
-  dif_chain<G, -1, true>(v, sm, t, a.tw);
+  dif_chain<G, -1, true>(v, sm, t, tws);
 
   double2 u[G::R / 2];
   if (!VAR) {
 #pragma unroll
-    for (int q = 0; q < G::R; ++q) v[q] = c_mul(v[q], __ldg(&a.mu[(t << k) | q]));
-    dit_chain<G, +1>(v, sm, t, a.tw);
+    for (int q = 0; q < G::R; ++q) v[q] = c_mul(v[q], a.mu[(t << k) | q]);
+    dit_chain<G, +1>(v, sm, t, tws);
   } else {
 #pragma unroll
     for (int q = 0; q < G::R; ++q) {
       const int s = (t << k) | q;
       smZ[s] = v[q];  // own positions: no barrier needed for the later reload
-      v[q] = c_scale(v[q], __ldg(&a.lamS[s]));
+      v[q] = c_scale(v[q], a.lamS[s]);
     }
-    dit_chain<G, +1>(v, sm, t, a.tw);
+    dit_chain<G, +1>(v, sm, t, tws);
 #pragma unroll
     for (int q = 0; q < G::R / 2; ++q) u[q] = v[q];
     __syncthreads();
@@ -122,55 +154,50 @@ k_toeplitz_lines(LineArgs a) {
     for (int q = 0; q < G::R; ++q) {
       const int s = (t << k) | q;
       const double2 z = smZ[s];
-      const double lk = __ldg(&a.lamK[s]);
+      const double lk = a.lamK[s];
       v[q] = make_double2(-lk * z.y, lk * z.x);  // i·Im λ ⊙ Z
     }
-    dit_chain<G, +1>(v, sm, t, a.tw);
+    dit_chain<G, +1>(v, sm, t, tws);
   }
 
 #pragma unroll
   for (int q = 0; q < G::R / 2; ++q) {
     const int p = (q << (K - k)) | t;
     if (p >= n) continue;
-    double o0 = 0.0, o1 = 0.0;
+    const long long o0 = A0.base + (long long)p * A0.stride, o1 = A1.base + (long long)p * A1.stride;
+    const int f0 = A0.fbase + p * A0.stride, f1 = A1.fbase + p * A1.stride;
+    double r0 = 0.0, r1 = 0.0;
     if (!VAR) {
-      o0 = v[q].x;
-      o1 = v[q].y;
+      r0 = v[q].x;
+      r1 = v[q].y;
       if (a.omul) {
-        if (v0) o0 *= __ldg(a.omul + LineAddr<COL>::fidx(l0, p, n, N));
-        if (v1) o1 *= __ldg(a.omul + LineAddr<COL>::fidx(l1, p, n, N));
+        if (v0) r0 *= __ldg(a.omul + f0);
+        if (v1) r1 *= __ldg(a.omul + f1);
       }
     } else {
-      if (v0) {
-        const int fi = LineAddr<COL>::fidx(l0, p, n, N);
-        o0 = __ldg(a.cP + fi) * u[q].x + __ldg(a.cM + fi) * v[q].x;
-      }
-      if (v1) {
-        const int fi = LineAddr<COL>::fidx(l1, p, n, N);
-        o1 = __ldg(a.cP + fi) * u[q].y + __ldg(a.cM + fi) * v[q].y;
-      }
+      if (v0) r0 = __ldg(a.cP + f0) * u[q].x + __ldg(a.cM + f0) * v[q].x;
+      if (v1) r1 = __ldg(a.cP + f1) * u[q].y + __ldg(a.cM + f1) * v[q].y;
     }
+    // ν x: folded into μ (ν + λ) for constant coefficients (the host passes
+    // nu = 0 then), explicit otherwise; the partial of the other direction is read here with
+    // plain loads (not hoisted above the transform by the compiler)
     if (v0) {
-      const long long o = LineAddr<COL>::off(l0, p, n, N);
-      double r = o0;
-      if (a.nu != 0.0) r = fma(a.nu, __ldg(a.x + o), r);
-      if (a.yin) r += __ldg(a.yin + o);
-      a.y[o] = r;
+      if (a.nu != 0.0) r0 = fma(a.nu, a.x[o0], r0);
+      if (a.yin) r0 += a.yin[o0];
+      a.y[o0] = r0;
     }
     if (v1) {
-      const long long o = LineAddr<COL>::off(l1, p, n, N);
-      double r = o1;
-      if (a.nu != 0.0) r = fma(a.nu, __ldg(a.x + o), r);
-      if (a.yin) r += __ldg(a.yin + o);
-      a.y[o] = r;
+      if (a.nu != 0.0) r1 = fma(a.nu, a.x[o1], r1);
+      if (a.yin) r1 += a.yin[o1];
+      a.y[o1] = r1;
     }
   }
 }
 
 // odd-extension loader: position p of the length-L odd extension of a line
 // (u_0 = u_m = 0, u_j = y_j, u_{L-j} = -y_j, j = 1..n; y_j is element j-1)
-template <bool COL>
-__device__ __forceinline__ double2 load_oddext(const LineArgs& a, int l0, int l1, bool v0, bool v1, int p, int m) {
+__device__ __forceinline__ double2 load_oddext(const LineArgs& a, const Line& A0, const Line& A1, bool v0, bool v1,
+                                               int p, int m) {
   int j = p;
   double sgn = 1.0;
   if (p > m) { j = 2 * m - p; sgn = -1.0; }
@@ -178,17 +205,29 @@ __device__ __forceinline__ double2 load_oddext(const LineArgs& a, int l0, int l1
   if (j >= 1 && j < m) {
     const int e = j - 1;
     if (v0) {
-      double val = __ldg(a.x + LineAddr<COL>::off(l0, e, a.n, a.N));
-      if (a.dpre) val *= __ldg(a.dpre + LineAddr<COL>::fidx(l0, e, a.n, a.N));
+      double val = __ldg(a.x + A0.base + (long long)e * A0.stride);
+      if (a.dpre) val *= __ldg(a.dpre + A0.fbase + e * A0.stride);
       re = sgn * val;
     }
     if (v1) {
-      double val = __ldg(a.x + LineAddr<COL>::off(l1, e, a.n, a.N));
-      if (a.dpre) val *= __ldg(a.dpre + LineAddr<COL>::fidx(l1, e, a.n, a.N));
+      double val = __ldg(a.x + A1.base + (long long)e * A1.stride);
+      if (a.dpre) val *= __ldg(a.dpre + A1.fbase + e * A1.stride);
       im = sgn * val;
     }
   }
   return make_double2(re, im);
+}
+
+__device__ __forceinline__ void store_pair(const LineArgs& a, const Line& A0, const Line& A1, bool v0, bool v1, int e,
+                                           double r0, double r1) {
+  if (v0) {
+    if (a.dpost) r0 *= __ldg(a.dpost + A0.fbase + e * A0.stride);
+    a.y[A0.base + (long long)e * A0.stride] = r0;
+  }
+  if (v1) {
+    if (a.dpost) r1 *= __ldg(a.dpost + A1.fbase + e * A1.stride);
+    a.y[A1.base + (long long)e * A1.stride] = r1;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -196,24 +235,32 @@ __device__ __forceinline__ double2 load_oddext(const LineArgs& a, int l0, int l1
 // folded into the τ multiplier), optional post-scale dpost.
 // ---------------------------------------------------------------------------
 template <int K, int k, bool COL, int FPC>
-__global__ void __launch_bounds__(FPC * (1 << (K - k)))
+__global__ void __launch_bounds__(FPC * (1 << (K - k)), min_blocks_for(FPC * (1 << (K - k))))
 k_dst_lines(LineArgs a) {
   using G = FftGeom<K, k>;
   using M = LineMap<G, COL, FPC>;
-  extern __shared__ double2 smem[];
+  extern __shared__ double2 smem_all[];
   if (a.gate && *a.gate == 0) return;
+  double2* sm_tw = smem_all;
+  double2* smem = smem_all + TW_SMEM_QUARTER * (G::L >> 2);
+  const TwSrc tws{sm_tw, a.twp};
   const int f = M::group(), t = M::lane();
   double2* sm = smem + (size_t)f * G::SM_STRIDE;
   const int g = blockIdx.x * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
+  const Line A0 = line_of<COL>(v0 ? l0 : 0, a.n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, a.n, a.N);
   constexpr int m = G::L / 2;
 
   double2 v[G::R];
 #pragma unroll
-  for (int q = 0; q < G::R; ++q) v[q] = load_oddext<COL>(a, l0, l1, v0, v1, (q << (K - k)) | t, m);
+  for (int q = 0; q < G::R; ++q) v[q] = load_oddext(a, A0, A1, v0, v1, (q << (K - k)) | t, m);
+  if (TW_SMEM_QUARTER) {
+    load_twiddles(sm_tw, a.tw, G::L);
+    __syncthreads();
+  }
 
-  dif_chain<G, -1, false>(v, sm, t, a.tw);
+  dif_chain<G, -1, false>(v, sm, t, tws);
   // permute bit-reversed -> natural through shared memory
   __syncthreads();
 #pragma unroll
@@ -228,19 +275,7 @@ k_dst_lines(LineArgs a) {
     const int fr = 1 + t + G::P * i;
     if (fr >= m) continue;
     const double2 U = sm[G::phys(fr)];
-    const int e = fr - 1;
-    if (v0) {
-      double r = -U.y;
-      const long long o = LineAddr<COL>::off(l0, e, a.n, a.N);
-      if (a.dpost) r *= __ldg(a.dpost + LineAddr<COL>::fidx(l0, e, a.n, a.N));
-      a.y[o] = r;
-    }
-    if (v1) {
-      double r = U.x;
-      const long long o = LineAddr<COL>::off(l1, e, a.n, a.N);
-      if (a.dpost) r *= __ldg(a.dpost + LineAddr<COL>::fidx(l1, e, a.n, a.N));
-      a.y[o] = r;
-    }
+    store_pair(a, A0, A1, v0, v1, fr - 1, -U.y, U.x);
   }
 }
 
@@ -254,28 +289,36 @@ k_dst_lines(LineArgs a) {
 // finishes the job.
 // ---------------------------------------------------------------------------
 template <int K, int k, bool COL, int FPC>
-__global__ void __launch_bounds__(FPC * (1 << (K - k)))
+__global__ void __launch_bounds__(FPC * (1 << (K - k)), min_blocks_for(FPC * (1 << (K - k))))
 k_tau_lines(LineArgs a) {
   using G = FftGeom<K, k>;
   using M = LineMap<G, COL, FPC>;
-  extern __shared__ double2 smem[];
+  extern __shared__ double2 smem_all[];
   if (a.gate && *a.gate == 0) return;
+  double2* sm_tw = smem_all;
+  double2* smem = smem_all + TW_SMEM_QUARTER * (G::L >> 2);
+  const TwSrc tws{sm_tw, a.twp};
   const int f = M::group(), t = M::lane();
   double2* sm = smem + (size_t)f * G::SM_STRIDE;
   const int g = blockIdx.x * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
+  const Line A0 = line_of<COL>(v0 ? l0 : 0, a.n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, a.n, a.N);
   constexpr int m = G::L / 2;
 
   double2 v[G::R];
 #pragma unroll
-  for (int q = 0; q < G::R; ++q) v[q] = load_oddext<COL>(a, l0, l1, v0, v1, (q << (K - k)) | t, m);
+  for (int q = 0; q < G::R; ++q) v[q] = load_oddext(a, A0, A1, v0, v1, (q << (K - k)) | t, m);
+  if (TW_SMEM_QUARTER) {
+    load_twiddles(sm_tw, a.tw, G::L);
+    __syncthreads();
+  }
 
-  dif_chain<G, -1, false>(v, sm, t, a.tw);
+  dif_chain<G, -1, false>(v, sm, t, tws);
 
   // x-frequency of this column pair (2D): both lines of a pair are columns c, c+1
-  const int c0 = COL ? (l0 % a.n) : 0;
-  const int c1 = COL ? ((v1 ? l1 : l0) % a.n) : 0;
+  const double fx0 = COL ? __ldg(a.Fx + A0.fbase) : 0.0;
+  const double fx1 = COL ? __ldg(a.Fx + (v1 ? A1.fbase : A0.fbase)) : 0.0;
 #pragma unroll
   for (int q = 0; q < G::R; ++q) {
     const int fr = bitrev_dev((t << k) | q, K);
@@ -283,43 +326,29 @@ k_tau_lines(LineArgs a) {
     double s0 = 0.0, s1 = 0.0;
     if (j >= 1 && j < m) {
       if (!COL) {
-        s0 = s1 = __ldg(a.invF + j - 1);
+        s0 = s1 = a.invF[j - 1];
       } else {
-        const double fy = __ldg(a.Fy + j - 1);
-        s0 = a.fscale / (__ldg(a.Fx + c0) + fy);
-        s1 = a.fscale / (__ldg(a.Fx + c1) + fy);
+        const double fy = a.Fy[j - 1];
+        s0 = a.fscale * fast_rcp(fx0 + fy);
+        s1 = a.fscale * fast_rcp(fx1 + fy);
       }
     }
-    // packed pair: V = i·s⊙U per line: line0 lives in the "-Im" channel and line1 in
-    // the "Re" channel; with distinct scales we treat them separately:
-    // U = 2c(F2 - i F1); V must equal i·(s0 F1' ... ) -> apply per-channel.
+    // packed pair U = DFT(oddext(r0 + i r1)): line 0's sine coefficients sit in
+    // -Im U, line 1's in Re U; V = (-s0·U.y) + i(s1·U.x) is the odd extension
+    // of the scaled coefficients of both lines, packed the same way.
     const double2 U = v[q];
-    // F1 ∝ -U.y, F2 ∝ U.x ; G1 = s0 F1, G2 = s1 F2 ; V = G1 + i G2 (odd-ext of G packed)
-    // in "U units": V = (-s0·U.y) + i (s1·U.x)
     v[q] = make_double2(-s0 * U.y, s1 * U.x);
   }
   // second forward DFT from bit-reversed input (DIT, sigma = -1)
   __syncthreads();
-  dit_chain<G, -1>(v, sm, t, a.tw);
+  dit_chain<G, -1>(v, sm, t, tws);
 
 #pragma unroll
   for (int q = 0; q < G::R / 2; ++q) {
     const int p = (q << (K - k)) | t;
     if (p < 1 || p >= m) continue;
-    const int e = p - 1;
     const double2 W = v[q];
-    if (v0) {
-      double r = -W.y;
-      const long long o = LineAddr<COL>::off(l0, e, a.n, a.N);
-      if (a.dpost) r *= __ldg(a.dpost + LineAddr<COL>::fidx(l0, e, a.n, a.N));
-      a.y[o] = r;
-    }
-    if (v1) {
-      double r = W.x;
-      const long long o = LineAddr<COL>::off(l1, e, a.n, a.N);
-      if (a.dpost) r *= __ldg(a.dpost + LineAddr<COL>::fidx(l1, e, a.n, a.N));
-      a.y[o] = r;
-    }
+    store_pair(a, A0, A1, v0, v1, p - 1, -W.y, W.x);
   }
 }
 

@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfde.so")
+LIB_PATH = os.environ.get("FDE_LIB") or os.path.join(_HERE, "libfde.so")
 
 FDE_OK = 0
 FDE_ERR_INVALID_ARG = 1
