@@ -1,0 +1,217 @@
+// DST-I and τ-solve line kernels on a complex FFT of length m = n+1
+// (SURVEY §7 hard part (a), route 1; P:L35 eq:sine_transform, P:L31 eq:tau).
+//
+// For a real line y_1..y_{m-1} (y_0 = y_m = 0) the sine sums
+// F_k = Σ_j y_j sin(πjk/m) follow from ONE real FFT of length m of
+//   w_j = sin(πj/m)(y_j + y_{m-j}) + ½(y_j − y_{m-j}),   j = 0..m-1,
+// W = FFT_m(w):  F_{2k} = −Im W_k,  F_1 = ½ Re W_0,  F_{2k+1} = F_{2k-1} + Re W_k.
+// Two lines are packed as w¹ + i w² into one complex FFT of length m and
+// separated with Z_k ± conj Z_{m-k}; the odd outputs are a prefix sum (a
+// group-wide scan, fixed order). Against the odd-extension FFT of length 2m
+// (k_dst_lines) this is 2.2x fewer butterflies per line. The kernels output
+// G = 2F = sqrt(2m)·(S_n y) like k_dst_lines, so the host scales (1/(2m) per
+// DST pair in the symbol divide) are unchanged.
+#pragma once
+#include "line_kernels.cuh"
+
+namespace fde {
+
+// Inclusive scan of two values over the lanes t = 0..P-1 of one line group
+// (lane layout of LineMap: rows tid = f·P + t, columns tid = t·FPC + f), via
+// warp shuffles within a segment and shared-memory segment totals. Returns
+// the exclusive prefix in (o0, o1). scr: FPC·(P/SEG)·2 doubles.
+template <bool COL, int P, int FPC>
+struct GroupScan {
+  static constexpr int SEG0 = COL ? 32 / FPC : (P < 32 ? P : 32);
+  static constexpr int SEG = SEG0 < 1 ? 1 : (SEG0 > P ? P : SEG0);
+  static constexpr int SUB = COL ? FPC : 1;
+  static constexpr int NSEG = P / SEG;
+  __device__ __forceinline__ static void excl(double x0, double x1, int t, int f, double* scr, double& o0, double& o1) {
+    const int pos = t % SEG;
+    double i0 = x0, i1 = x1;
+#pragma unroll
+    for (int d = 1; d < SEG; d <<= 1) {
+      const double y0 = __shfl_up_sync(0xffffffffu, i0, d * SUB);
+      const double y1 = __shfl_up_sync(0xffffffffu, i1, d * SUB);
+      if (pos >= d) {
+        i0 += y0;
+        i1 += y1;
+      }
+    }
+    if (pos == SEG - 1) {
+      scr[(f * NSEG + t / SEG) * 2 + 0] = i0;
+      scr[(f * NSEG + t / SEG) * 2 + 1] = i1;
+    }
+    __syncthreads();
+    double s0 = 0.0, s1 = 0.0;
+    for (int s = 0; s < t / SEG; ++s) {
+      s0 += scr[(f * NSEG + s) * 2 + 0];
+      s1 += scr[(f * NSEG + s) * 2 + 1];
+    }
+    o0 = s0 + (i0 - x0);
+    o1 = s1 + (i1 - x1);
+  }
+};
+
+// One packed-pair DST after the FFT: v holds Z = FFT_m(w¹ + i w²) in the
+// DIF output layout. Leaves g0[i], g1[i] = G_idx of line 0/1 for the 2C
+// consecutive indices idx = 2Ct + i (idx 0 is meaningless), C = m/(2P).
+template <class G, bool COL, int FPC>
+__device__ __forceinline__ void dstm_post(double2 (&v)[G::R], double2* sm, double* scr, int t, int f,
+                                          double (&g0)[G::R], double (&g1)[G::R]) {
+  constexpr int m = G::L, P = G::P, k = G::k, C = G::R / 2;
+  __syncthreads();  // the chain's last exchange reads are done
+#pragma unroll
+  for (int q = 0; q < G::R; ++q) sm[G::phys(bitrev_dev((t << k) | q, G::K))] = v[q];
+  __syncthreads();
+  double re0[C], re1[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int kk = C * t + c;
+    const double2 Zk = sm[G::phys(kk)];
+    const double2 Zm = sm[G::phys((m - kk) & (m - 1))];
+    // V1 = Z_k + conj Z_{m-k} (= 2W¹_k), V2 = -i(Z_k - conj Z_{m-k}) (= 2W²_k)
+    g0[2 * c] = Zm.y - Zk.y;    // G_{2kk} = -Im V1
+    g1[2 * c] = Zk.x - Zm.x;    // G_{2kk} = -Im V2
+    re0[c] = Zk.x + Zm.x;       // Re V1
+    re1[c] = Zk.y + Zm.y;       // Re V2
+  }
+  // Re V_0 of both lines (lane 0 holds kk = 0): G_1 = ½ Re V_0, G_{2k+1} = G_{2k-1} + Re V_k
+  double* v0s = scr + FPC * GroupScan<COL, P, FPC>::NSEG * 2;
+  if (t == 0) {
+    v0s[2 * f + 0] = re0[0];
+    v0s[2 * f + 1] = re1[0];
+  }
+#pragma unroll
+  for (int c = 1; c < C; ++c) {
+    re0[c] += re0[c - 1];
+    re1[c] += re1[c - 1];
+  }
+  double o0, o1;
+  GroupScan<COL, P, FPC>::excl(re0[C - 1], re1[C - 1], t, f, scr, o0, o1);  // contains a barrier
+  o0 -= 0.5 * v0s[2 * f + 0];
+  o1 -= 0.5 * v0s[2 * f + 1];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    g0[2 * c + 1] = o0 + re0[c];
+    g1[2 * c + 1] = o1 + re1[c];
+  }
+}
+
+// w_j of the packed pair from values y_j, y_{m-j} of both lines
+__device__ __forceinline__ double2 dstm_pre(double sj, double a0, double b0, double a1, double b1) {
+  return make_double2(fma(sj, a0 + b0, 0.5 * (a0 - b0)), fma(sj, a1 + b1, 0.5 * (a1 - b1)));
+}
+
+// ---------------------------------------------------------------------------
+// TAU = false: raw DST-I along lines, out = dpost ⊙ G(dpre ⊙ y).
+// TAU = true : the τ core along lines, out = dpost ⊙ G(s ⊙ G(dpre ⊙ y)) with
+//              s = invF (1D rows) or fscale / (Fx_col + Fy_j) (2D columns).
+// ---------------------------------------------------------------------------
+template <int KM, int k, bool COL, int FPC, bool TAU>
+__global__ void __launch_bounds__(FPC * (1 << (KM - k)), min_blocks_for(FPC * (1 << (KM - k))))
+k_dstm_lines(LineArgs a) {
+  using G = FftGeom<KM, k>;
+  using M = LineMap<G, COL, FPC>;
+  constexpr int m = G::L, P = G::P, R = G::R, C = R / 2;
+  extern __shared__ double2 smem_all[];
+  if (a.gate && *a.gate == 0) return;
+  const int f = M::group(), t = M::lane();
+  double2* sm = smem_all + (size_t)f * G::SM_STRIDE;
+  double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * G::SM_STRIDE);
+  const TwSrc tws{nullptr, a.twpm};
+  const int g = blockIdx.x * FPC + f;
+  const int l0 = 2 * g, l1 = 2 * g + 1;
+  const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
+  const Line A0 = line_of<COL>(v0 ? l0 : 0, a.n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, a.n, a.N);
+
+  double2 v[R];
+  // pre-process from global: position j = (q << (KM-k)) | t of the DIF input
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int j = (q << (KM - k)) | t;
+    double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+    if (j >= 1) {
+      const int e1 = j - 1, e2 = m - j - 1;
+      if (v0) {
+        a0 = __ldg(a.x + A0.base + (long long)e1 * A0.stride);
+        b0 = __ldg(a.x + A0.base + (long long)e2 * A0.stride);
+        if (a.dpre) {
+          a0 *= __ldg(a.dpre + A0.fbase + e1 * A0.stride);
+          b0 *= __ldg(a.dpre + A0.fbase + e2 * A0.stride);
+        }
+      }
+      if (v1) {
+        a1 = __ldg(a.x + A1.base + (long long)e1 * A1.stride);
+        b1 = __ldg(a.x + A1.base + (long long)e2 * A1.stride);
+        if (a.dpre) {
+          a1 *= __ldg(a.dpre + A1.fbase + e1 * A1.stride);
+          b1 *= __ldg(a.dpre + A1.fbase + e2 * A1.stride);
+        }
+      }
+    }
+    v[q] = dstm_pre(__ldg(a.sinm + j), a0, b0, a1, b1);
+  }
+  dif_chain<G, -1, false>(v, sm, t, tws);
+  double g0[R], g1[R];
+  dstm_post<G, COL, FPC>(v, sm, scr, t, f, g0, g1);
+
+  if (TAU) {
+    // symbol divide (normalisation folded), then the second DST from shared memory
+    const double fx0 = COL ? __ldg(a.Fx + A0.fbase) : 0.0;
+    const double fx1 = COL ? __ldg(a.Fx + (v1 ? A1.fbase : A0.fbase)) : 0.0;
+    __syncthreads();  // Z reads of dstm_post are done
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int idx = 2 * C * t + i;
+      if (idx < 1) continue;
+      double s0, s1;
+      if (!COL) {
+        s0 = s1 = a.invF[idx - 1];
+      } else {
+        const double fy = a.Fy[idx - 1];
+        s0 = a.fscale * fast_rcp(fx0 + fy);
+        s1 = a.fscale * fast_rcp(fx1 + fy);
+      }
+      sm[G::phys(idx)] = make_double2(s0 * g0[i], s1 * g1[i]);
+    }
+    if (t == 0) sm[G::phys(0)] = make_double2(0.0, 0.0);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int j = (q << (KM - k)) | t;
+      const double2 yj = sm[G::phys(j)];
+      const double2 ym = sm[G::phys((m - j) & (m - 1))];   // j = 0: both are entry 0 = 0
+      v[q] = dstm_pre(__ldg(a.sinm + j), yj.x, ym.x, yj.y, ym.y);
+    }
+    __syncthreads();  // the chain's first exchange overwrites sm
+    dif_chain<G, -1, false>(v, sm, t, tws);
+    dstm_post<G, COL, FPC>(v, sm, scr, t, f, g0, g1);
+  }
+
+  if (COL) {
+    // each lane owns 2C consecutive rows: the FPC interleaved groups of a warp
+    // write the same rows of adjacent columns together
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int idx = 2 * C * t + i;
+      if (idx >= 1) store_pair(a, A0, A1, v0, v1, idx - 1, g0[i], g1[i]);
+    }
+  } else {
+    // rows: stage through shared memory for coalesced stores
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < R; ++i) sm[G::phys(2 * C * t + i)] = make_double2(g0[i], g1[i]);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int e = t + P * i;
+      if (e < m - 1) {
+        const double2 o = sm[G::phys(e + 1)];
+        store_pair(a, A0, A1, v0, v1, e, o.x, o.y);
+      }
+    }
+  }
+}
+
+}  // namespace fde

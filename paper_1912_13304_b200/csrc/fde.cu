@@ -21,6 +21,7 @@
 #include "../../include/fde.h"
 #include "krylov_kernels.cuh"
 #include "line_kernels.cuh"
+#include "dst_kernels.cuh"
 
 using namespace fde;
 
@@ -128,6 +129,26 @@ int bitrev_host(int x, int bits) {
   return r;
 }
 
+// per-pass twiddle table of the FFT engine (fft_engine.cuh, FDE_TW_MODE 1):
+// entry [pass I][q][t_lo] = W_{2^K}^{(t_lo << (K-lo-ka)) bitrev_ka(q)}
+std::vector<double2> pass_twiddles_host(int K, int k) {
+  std::vector<double2> tp;
+  const long long L = 1LL << K;
+  for (int I = 0; I * k < K; ++I) {
+    const int lo = K - (I + 1) * k > 0 ? K - (I + 1) * k : 0;
+    const int ka = K - I * k - lo;
+    if (lo == 0) break;
+    for (int q = 0; q < (1 << k); ++q)
+      for (int tl = 0; tl < (1 << lo); ++tl) {
+        const long long e = q < (1 << ka) ? ((long long)tl << (K - lo - ka)) * bitrev_host(q, ka) : 0;
+        auto z = root_of_unity(e, L);
+        tp.push_back(make_double2(z.real(), z.imag()));
+      }
+  }
+  if (tp.empty()) tp.push_back(make_double2(1.0, 0.0));
+  return tp;
+}
+
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
@@ -152,6 +173,19 @@ struct LaunchCfg {
   static constexpr bool FITS = SPG + TW_SMEM_QUARTER * (G::L / 4) * 16 <= 227 * 1024;
 };
 
+// DST/τ kernels on the length-m FFT (dst_kernels.cuh)
+template <int KM, bool COL>
+struct LaunchCfgM {
+  using G = FftGeom<KM, KR>;
+  static constexpr int SPG = G::SM_STRIDE * 16;
+  static constexpr int BY_THR = 512 / G::P > 0 ? 512 / G::P : 1;
+  static constexpr int WANT = COL ? (128 / G::P > 2 ? 128 / G::P : 2) : (128 / G::P > 1 ? 128 / G::P : 1);
+  static constexpr int FPC = WANT < BY_THR ? WANT : BY_THR;
+  static constexpr int THREADS = FPC * G::P;
+  static constexpr int SCR = (FPC * (GroupScan<COL, G::P, FPC>::NSEG + 1) * 2) * 8;
+  static constexpr int SMEM = FPC * SPG + SCR;
+};
+
 }  // namespace
 
 // ======================================================================== handle
@@ -166,6 +200,8 @@ struct fde_handle_s {
   // tables
   double2* tw = nullptr;
   double2* twp = nullptr;
+  double2* twpm = nullptr;
+  double* sinm = nullptr;
   double2 *mu_x = nullptr, *mu_y = nullptr;
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
   double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
@@ -224,6 +260,8 @@ LineArgs base_args(fde_handle h) {
   a.N = h->N;
   a.tw = h->tw;
   a.twp = h->twp;
+  a.twpm = h->twpm;
+  a.sinm = h->sinm;
   return a;
 }
 
@@ -275,6 +313,15 @@ void launch_tau_k(fde_handle h, const LineArgs& a) {
                [&] { kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a); });
 }
 
+template <int KM, bool COL, bool TAU>
+void launch_dstm_k(fde_handle h, const LineArgs& a) {
+  using C = LaunchCfgM<KM, COL>;
+  auto kern = k_dstm_lines<KM, KR, COL, C::FPC, TAU>;
+  const int npairs = (a.nlines + 1) / 2;
+  launch_named(h, TAU ? (COL ? "tau_cols" : "tau_rows") : (COL ? "dst_cols" : "dst_rows"),
+               [&] { kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a); });
+}
+
 #define FDE_SWITCH_K(K, CALL)                                           \
   switch (K) {                                                          \
     case 6: { constexpr int KK = 6; CALL; } break;                      \
@@ -304,11 +351,13 @@ void init_kernel_attrs() {
   set_attr_toep<K, true, false>();
   set_attr_toep<K, false, true>();
   set_attr_toep<K, true, true>();
+  using D0 = LaunchCfgM<K - 1, false>;
+  using D1 = LaunchCfgM<K - 1, true>;
+  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KR, false, D0::FPC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
+  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KR, false, D0::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
+  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KR, true, D1::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D1::SMEM));
   using C0 = LaunchCfg<K, false, 1>;
   using C1 = LaunchCfg<K, true, 1>;
-  FDE_CUDA(cudaFuncSetAttribute(k_dst_lines<K, KR, false, C0::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C0::SMEM));
-  FDE_CUDA(cudaFuncSetAttribute(k_tau_lines<K, KR, false, C0::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C0::SMEM));
-  FDE_CUDA(cudaFuncSetAttribute(k_tau_lines<K, KR, true, C1::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM));
 }
 
 // One Toeplitz pass along rows (COL=false) or columns (COL=true).
@@ -391,7 +440,7 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate) {
     a.invF = h->invF;
     a.dpre = h->dpre;
     a.dpost = h->dpost;
-    FDE_SWITCH_K(h->K, (launch_tau_k<KK, false>(h, a)));
+    FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, true>(h, a)));
     return;
   }
   // 2D: rows DST (pre-scale) -> columns DST·F⁻¹·DST -> rows DST (post-scale)
@@ -399,7 +448,7 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate) {
   a.x = r;
   a.y = h->t1;
   a.dpre = h->dpre;
-  FDE_SWITCH_K(h->K, (launch_dst_k<KK, false>(h, a)));
+  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, a)));
   LineArgs b = base_args(h);
   b.gate = gate;
   b.nlines = h->batch * h->n;
@@ -408,14 +457,14 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate) {
   b.Fx = h->Fx;
   b.Fy = h->Fy;
   b.fscale = h->fscale;
-  FDE_SWITCH_K(h->K, (launch_tau_k<KK, true>(h, b)));
+  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, true, true>(h, b)));
   LineArgs c = base_args(h);
   c.gate = gate;
   c.nlines = h->batch * h->n;
   c.x = h->t2;
   c.y = z;
   c.dpost = h->dpost;
-  FDE_SWITCH_K(h->K, (launch_dst_k<KK, false>(h, c)));
+  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, c)));
 }
 
 // ------------------------------------------------------------- create
@@ -459,22 +508,13 @@ void build(fde_handle h, const fde_desc* d) {
   std::vector<double2> tw(L / 4);
   for (int e = 0; e < L / 4; ++e) { auto z = root_of_unity(e, L); tw[e] = make_double2(z.real(), z.imag()); }
   h->tw = h->upload(tw);
-  {  // per-pass twiddle tables (FDE_TW_MODE 1): [pass I][q][t_lo] = W_L^{(t_lo << (K-lo-ka)) bitrev_ka(q)}
-    const int K = h->K, k = KR;
-    std::vector<double2> tp;
-    for (int I = 0; (I * k) < K; ++I) {
-      const int lo = K - (I + 1) * k > 0 ? K - (I + 1) * k : 0;
-      const int ka = K - I * k - lo;
-      if (lo == 0) break;
-      for (int q = 0; q < (1 << k); ++q)
-        for (int tl = 0; tl < (1 << lo); ++tl) {
-          const long long e = q < (1 << ka) ? ((long long)tl << (K - lo - ka)) * bitrev_host(q, ka) : 0;
-          auto z = root_of_unity(e, L);
-          tp.push_back(make_double2(z.real(), z.imag()));
-        }
-    }
-    if (tp.empty()) tp.push_back(make_double2(1.0, 0.0));
-    h->twp = h->upload(tp);
+  // per-pass twiddle tables of the length-L (Toeplitz) and length-m (DST) FFTs
+  h->twp = h->upload(pass_twiddles_host(h->K, KR));
+  h->twpm = h->upload(pass_twiddles_host(h->K - 1, KR));
+  {
+    std::vector<double> sv(m);
+    for (int j = 0; j < m; ++j) sv[j] = std::sin(M_PI * (double)std::min(j, m - j) / (double)m);  // sin(πj/m)
+    h->sinm = h->upload(sv);
   }
 
   // circulant eigenvalues λ = DFT_L(c), c = first column of the embedding

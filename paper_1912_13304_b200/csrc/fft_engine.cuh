@@ -189,22 +189,35 @@ __host__ __device__ constexpr int tw_pass_offset(int I) {
   }
   return o;
 }
-template <class G, int I, int SIGMA>
-__device__ __forceinline__ void pass_twiddles(double2 (&v)[G::R], int t, const TwSrc& tw) {
+// Twiddles of pass I for thread t, read into registers (plain loads, so the
+// compiler keeps them where they are written: the chains issue them BEFORE the
+// shared-memory exchange that precedes the pass, hiding their latency).
+#ifndef FDE_TW_PREFETCH
+#define FDE_TW_PREFETCH 0   // 1: issue a pass's twiddle loads before the exchange that precedes it
+#endif
+template <class G>
+struct PassTw {
+  double2 w[G::R];
+};
+template <class G, int I>
+__device__ __forceinline__ void load_pass_tw(PassTw<G>& pt, int t, const TwSrc& tw) {
   constexpr int l = G::lo(I), a = G::ka(I);
   if (l == 0) return;
-#if FDE_TW_MODE == 0
-  apply_twiddles<G::k, a, SIGMA>(v, base_exponent<G, I>(t), G::L, tw.sm);
-#else
   const double2* tp = tw.gp + tw_pass_offset<G::K, G::k>(I) + (t & ((1 << l) - 1));
 #pragma unroll
-  for (int q = 1; q < (1 << a); ++q) v[q] = c_mul_tw<SIGMA>(v[q], tp[q << l]);  // plain load: stays below the barrier
-#endif
+  for (int q = 1; q < (1 << a); ++q) pt.w[q] = tp[q << l];
+}
+template <class G, int I, int SIGMA>
+__device__ __forceinline__ void pass_twiddles(double2 (&v)[G::R], const PassTw<G>& pt) {
+  constexpr int l = G::lo(I), a = G::ka(I);
+  if (l == 0) return;
+#pragma unroll
+  for (int q = 1; q < (1 << a); ++q) v[q] = c_mul_tw<SIGMA>(v[q], pt.w[q]);
 }
 
 // DIF pass I on registers (no memory traffic).
 template <class G, int I, int SIGMA, bool HALF_ZERO>
-__device__ __forceinline__ void dif_pass(double2 (&v)[G::R], int t, const TwSrc& tw) {
+__device__ __forceinline__ void dif_pass(double2 (&v)[G::R], const PassTw<G>& tw) {
   constexpr int a = G::ka(I);
   if (HALF_ZERO && a == G::k) {
     // upper half of the inputs are zero: first radix-2 stage is a copy/twiddle
@@ -226,13 +239,13 @@ __device__ __forceinline__ void dif_pass(double2 (&v)[G::R], int t, const TwSrc&
   } else {
     dft_dif<G::k, a, SIGMA>(v);
   }
-  pass_twiddles<G, I, SIGMA>(v, t, tw);
+  pass_twiddles<G, I, SIGMA>(v, tw);
 }
 
 template <class G, int I, int SIGMA>
-__device__ __forceinline__ void dit_pass(double2 (&v)[G::R], int t, const TwSrc& tw) {
+__device__ __forceinline__ void dit_pass(double2 (&v)[G::R], const PassTw<G>& tw) {
   constexpr int a = G::ka(I);
-  pass_twiddles<G, I, SIGMA>(v, t, tw);
+  pass_twiddles<G, I, SIGMA>(v, tw);
   dft_dit<G::k, a, SIGMA>(v);
 }
 
@@ -251,12 +264,15 @@ __device__ __forceinline__ void sm_load(const double2* sm, double2 (&v)[G::R], i
 template <class G, int I, int SIGMA, bool HALF_ZERO>
 struct DifChain {
   __device__ __forceinline__ static void run(double2 (&v)[G::R], double2* sm, int t, const TwSrc& tw) {
+    PassTw<G> pt;
+    if (FDE_TW_PREFETCH) load_pass_tw<G, I>(pt, t, tw);
     if (I > 0) {
       sm_store<G>(sm, v, t, I - 1);
       __syncthreads();
       sm_load<G>(sm, v, t, I);
     }
-    dif_pass<G, I, SIGMA, (I == 0) && HALF_ZERO>(v, t, tw);
+    if (!FDE_TW_PREFETCH) load_pass_tw<G, I>(pt, t, tw);
+    dif_pass<G, I, SIGMA, (I == 0) && HALF_ZERO>(v, pt);
     DifChain<G, I + 1, SIGMA, HALF_ZERO>::run(v, sm, t, tw);
   }
 };
@@ -268,12 +284,15 @@ struct DifChain<G, G::NP, SIGMA, HALF_ZERO> {
 template <class G, int I, int SIGMA>
 struct DitChain {  // runs passes I, I-1, ..., 0
   __device__ __forceinline__ static void run(double2 (&v)[G::R], double2* sm, int t, const TwSrc& tw) {
+    PassTw<G> pt;
+    if (FDE_TW_PREFETCH) load_pass_tw<G, I>(pt, t, tw);
     if (I < G::NP - 1) {
       sm_store<G>(sm, v, t, I + 1);
       __syncthreads();
       sm_load<G>(sm, v, t, I);
     }
-    dit_pass<G, I, SIGMA>(v, t, tw);
+    if (!FDE_TW_PREFETCH) load_pass_tw<G, I>(pt, t, tw);
+    dit_pass<G, I, SIGMA>(v, pt);
     DitChain<G, I - 1, SIGMA>::run(v, sm, t, tw);
   }
 };

@@ -26,7 +26,9 @@ struct LineArgs {
   int N;                  // elements per RHS (n or n*n)
   double nu;              // shift ν·x added to the output (0 to skip)
   const double2* tw;      // quarter twiddle table exp(-2 pi i r/L), r < L/4 (FDE_TW_MODE 0)
-  const double2* twp;     // per-pass twiddle tables (FDE_TW_MODE 1, fft_engine.cuh)
+  const double2* twp;     // per-pass twiddle tables of the length-L FFT (fft_engine.cuh)
+  const double2* twpm;    // per-pass twiddle tables of the length-m FFT (dst_kernels.cuh)
+  const double* sinm;     // sin(πj/m), j = 0..m-1 (dst_kernels.cuh)
   const double2* mu;      // const Toeplitz: complex multiplier, bit-reversed order, 1/L folded
   const double* lamS;     // variable Toeplitz: Re λ / L (bit-reversed order)
   const double* lamK;     // variable Toeplitz: Im λ / L (bit-reversed order)
