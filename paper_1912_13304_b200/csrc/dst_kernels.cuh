@@ -103,6 +103,22 @@ __device__ __forceinline__ double2 dstm_pre(double sj, double a0, double b0, dou
   return make_double2(fma(sj, a0 + b0, 0.5 * (a0 - b0)), fma(sj, a1 + b1, 0.5 * (a1 - b1)));
 }
 
+// w of the packed pair for the DIF input positions j = (q << (KM-k)) | t from
+// the natural-order line pair in shared memory (sm[phys(0)] = 0); ends with a
+// barrier because the chain's first exchange overwrites sm.
+template <class G, int KM, int k>
+__device__ __forceinline__ void dstm_pre_smem(double2 (&v)[G::R], const double2* sm, int t, const double* sinm) {
+  constexpr int m = G::L;
+#pragma unroll
+  for (int q = 0; q < G::R; ++q) {
+    const int j = (q << (KM - k)) | t;
+    const double2 yj = sm[G::phys(j)];
+    const double2 ym = sm[G::phys((m - j) & (m - 1))];   // j = 0: both are entry 0 = 0
+    v[q] = dstm_pre(__ldg(sinm + j), yj.x, ym.x, yj.y, ym.y);
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // TAU = false: raw DST-I along lines, out = dpost ⊙ G(dpre ⊙ y).
 // TAU = true : the τ core along lines, out = dpost ⊙ G(s ⊙ G(dpre ⊙ y)) with
@@ -116,6 +132,8 @@ k_dstm_lines(LineArgs a) {
   constexpr int m = G::L, P = G::P, R = G::R, C = R / 2;
   extern __shared__ double2 smem_all[];
   if (a.gate && *a.gate == 0) return;
+  if (kry_skip(a)) return;
+  FDE_PROBE(0);
   const int f = M::group(), t = M::lane();
   double2* sm = smem_all + (size_t)f * G::SM_STRIDE;
   double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * G::SM_STRIDE);
@@ -123,38 +141,55 @@ k_dstm_lines(LineArgs a) {
   const int g = blockIdx.x * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
-  const Line A0 = line_of<COL>(v0 ? l0 : 0, a.n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, a.n, a.N);
+  const Line A0 = line_of<COL>(v0 ? l0 : 0, blockIdx.y, a.n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, blockIdx.y, a.n, a.N);
 
   double2 v[R];
-  // pre-process from global: position j = (q << (KM-k)) | t of the DIF input
+  // stage both lines in shared memory in natural order (position j = element
+  // j-1; positions 0 and m are the zero boundary values), one coalesced load
+  // per element, dpre applied on the way
+  double acc[3] = {0.0, 0.0, 0.0};
+  const bool xr = (a.kf.mode & KM_XR) != 0, rz = (a.kf.mode & KM_RZ) != 0;
+  const double alpha = xr ? a.kf.st[blockIdx.y].alpha : 0.0;
 #pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const int j = (q << (KM - k)) | t;
-    double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
-    if (j >= 1) {
-      const int e1 = j - 1, e2 = m - j - 1;
-      if (v0) {
-        a0 = __ldg(a.x + A0.base + (long long)e1 * A0.stride);
-        b0 = __ldg(a.x + A0.base + (long long)e2 * A0.stride);
-        if (a.dpre) {
-          a0 *= __ldg(a.dpre + A0.fbase + e1 * A0.stride);
-          b0 *= __ldg(a.dpre + A0.fbase + e2 * A0.stride);
+  for (int i = 0; i < R; ++i) {
+    const int e = t + P * i;
+    if (e < m - 1) {
+      double y0 = 0.0, y1 = 0.0;
+      const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
+      if (xr) {  // x += α p, r -= α q (KM_XR; a.x = r), ‖r‖² partial
+        if (v0) {
+          y0 = fma(-alpha, a.kf.q[o0], a.kf.r[o0]);
+          a.kf.r[o0] = y0;
+          a.kf.x[o0] = fma(alpha, a.kf.p[o0], a.kf.x[o0]);
+          acc[1] = fma(y0, y0, acc[1]);
         }
-      }
-      if (v1) {
-        a1 = __ldg(a.x + A1.base + (long long)e1 * A1.stride);
-        b1 = __ldg(a.x + A1.base + (long long)e2 * A1.stride);
-        if (a.dpre) {
-          a1 *= __ldg(a.dpre + A1.fbase + e1 * A1.stride);
-          b1 *= __ldg(a.dpre + A1.fbase + e2 * A1.stride);
+        if (v1) {
+          y1 = fma(-alpha, a.kf.q[o1], a.kf.r[o1]);
+          a.kf.r[o1] = y1;
+          a.kf.x[o1] = fma(alpha, a.kf.p[o1], a.kf.x[o1]);
+          acc[1] = fma(y1, y1, acc[1]);
         }
+      } else {
+        if (v0) y0 = __ldg(a.x + o0);
+        if (v1) y1 = __ldg(a.x + o1);
       }
+      if (a.dpre) {
+        if (v0) y0 *= __ldg(a.dpre + A0.fbase + e * A0.stride);
+        if (v1) y1 *= __ldg(a.dpre + A1.fbase + e * A1.stride);
+      }
+      sm[G::phys(e + 1)] = make_double2(y0, y1);
     }
-    v[q] = dstm_pre(__ldg(a.sinm + j), a0, b0, a1, b1);
   }
+  if (t == 0) sm[G::phys(0)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  dstm_pre_smem<G, KM, k>(v, sm, t, a.sinm);
+  __syncwarp();
+  FDE_PROBE(1);
   dif_chain<G, -1, false>(v, sm, t, tws);
+  FDE_PROBE(2);
   double g0[R], g1[R];
   dstm_post<G, COL, FPC>(v, sm, scr, t, f, g0, g1);
+  FDE_PROBE(3);
 
   if (TAU) {
     // symbol divide (normalisation folded), then the second DST from shared memory
@@ -177,14 +212,7 @@ k_dstm_lines(LineArgs a) {
     }
     if (t == 0) sm[G::phys(0)] = make_double2(0.0, 0.0);
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int j = (q << (KM - k)) | t;
-      const double2 yj = sm[G::phys(j)];
-      const double2 ym = sm[G::phys((m - j) & (m - 1))];   // j = 0: both are entry 0 = 0
-      v[q] = dstm_pre(__ldg(a.sinm + j), yj.x, ym.x, yj.y, ym.y);
-    }
-    __syncthreads();  // the chain's first exchange overwrites sm
+    dstm_pre_smem<G, KM, k>(v, sm, t, a.sinm);
     dif_chain<G, -1, false>(v, sm, t, tws);
     dstm_post<G, COL, FPC>(v, sm, scr, t, f, g0, g1);
   }
@@ -209,9 +237,17 @@ k_dstm_lines(LineArgs a) {
       if (e < m - 1) {
         const double2 o = sm[G::phys(e + 1)];
         store_pair(a, A0, A1, v0, v1, e, o.x, o.y);
+        if (rz) {  // r·z partial of the stored z (KM_RZ)
+          const double z0 = a.dpost ? o.x * __ldg(a.dpost + A0.fbase + e * A0.stride) : o.x;
+          const double z1 = a.dpost ? o.y * __ldg(a.dpost + A1.fbase + e * A1.stride) : o.y;
+          if (v0) acc[2] = fma(a.kf.r[A0.base + (long long)e * A0.stride], z0, acc[2]);
+          if (v1) acc[2] = fma(a.kf.r[A1.base + (long long)e * A1.stride], z1, acc[2]);
+        }
       }
     }
   }
+  FDE_PROBE(4);
+  if (xr || rz) kry_reduce_finalize(a.kf, acc);
 }
 
 }  // namespace fde

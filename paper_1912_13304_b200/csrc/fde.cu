@@ -48,7 +48,11 @@ struct FdeFail {
 #ifndef FDE_KR
 #define FDE_KR 4
 #endif
-constexpr int KMIN = 6, KMAX = 13, KR = FDE_KR;  // log2 points per thread in the FFT engine
+#ifndef FDE_KRM
+#define FDE_KRM 3
+#endif
+constexpr int KMIN = 6, KMAX = 13, KR = FDE_KR;  // log2 points per thread in the FFT engine (length-L FFTs)
+constexpr int KRM = FDE_KRM;                      // same for the length-m FFTs of the DST kernels
 
 // ------------------------------------------------------------------ host maths
 std::vector<double> grunwald(double alpha, int K) {  // g_k = (-1)^k C(α,k)
@@ -159,7 +163,7 @@ bool is_device_ptr(const void* p) {
 template <int K, bool COL, int NBUF>
 struct LaunchCfg {
   using G = FftGeom<K, KR>;
-  static constexpr int SPG = G::SM_STRIDE * 16 * NBUF;      // smem bytes per FFT group
+  static constexpr int SPG = G::SM_STRIDE * 16 * NBUF + (COL ? (G::L / 2) * 16 : 0);  // smem bytes per FFT group (+ yin staging)
   static constexpr int SMEM_CAP = 200 * 1024;
   static constexpr int BY_SMEM = (SMEM_CAP - TW_SMEM_QUARTER * (G::L / 4) * 16) / SPG > 0 ? (SMEM_CAP - TW_SMEM_QUARTER * (G::L / 4) * 16) / SPG : 1;
   static constexpr int BY_THR = 512 / G::P > 0 ? 512 / G::P : 1;  // <= 512 threads: 128 registers/thread
@@ -176,10 +180,10 @@ struct LaunchCfg {
 // DST/τ kernels on the length-m FFT (dst_kernels.cuh)
 template <int KM, bool COL>
 struct LaunchCfgM {
-  using G = FftGeom<KM, KR>;
+  using G = FftGeom<KM, KRM>;
   static constexpr int SPG = G::SM_STRIDE * 16;
   static constexpr int BY_THR = 512 / G::P > 0 ? 512 / G::P : 1;
-  static constexpr int WANT = COL ? (128 / G::P > 2 ? 128 / G::P : 2) : (128 / G::P > 1 ? 128 / G::P : 1);
+  static constexpr int WANT = COL ? (64 / G::P > 2 ? 64 / G::P : 2) : (64 / G::P > 1 ? 64 / G::P : 1);
   static constexpr int FPC = WANT < BY_THR ? WANT : BY_THR;
   static constexpr int THREADS = FPC * G::P;
   static constexpr int SCR = (FPC * (GroupScan<COL, G::P, FPC>::NSEG + 1) * 2) * 8;
@@ -218,6 +222,7 @@ struct fde_handle_s {
   Counters* ctr = nullptr;
   double* part = nullptr;
   double *kx = nullptr, *kb = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kq = nullptr;
+  double* kpart = nullptr;  // fused-kernel partials [batch][3][KPMAX]
   double* V = nullptr;
   int V_cols = 0;
   // graphs
@@ -253,6 +258,9 @@ struct fde_handle_s {
 
 namespace {
 
+#ifdef FDE_PROBES
+int g_probe_next = 0;
+#endif
 LineArgs base_args(fde_handle h) {
   LineArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -262,6 +270,9 @@ LineArgs base_args(fde_handle h) {
   a.twp = h->twp;
   a.twpm = h->twpm;
   a.sinm = h->sinm;
+#ifdef FDE_PROBES
+  a.probe = g_probe_next++ & 7;
+#endif
   return a;
 }
 
@@ -292,34 +303,18 @@ void launch_toep_k(fde_handle h, const LineArgs& a) {
   using C = LaunchCfg<K, COL, VAR ? 2 : 1>;
   auto kern = k_toeplitz_lines<K, KR, COL, VAR, C::FPC>;
   const int npairs = (a.nlines + 1) / 2;
-  const int grid = (npairs + C::FPC - 1) / C::FPC;
+  const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
   launch_named(h, COL ? (VAR ? "toeplitz_cols_var" : "toeplitz_cols") : (VAR ? "toeplitz_rows_var" : "toeplitz_rows"),
                [&] { kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a); });
 }
-template <int K, bool COL>
-void launch_dst_k(fde_handle h, const LineArgs& a) {
-  using C = LaunchCfg<K, COL, 1>;
-  auto kern = k_dst_lines<K, KR, COL, C::FPC>;
-  const int npairs = (a.nlines + 1) / 2;
-  launch_named(h, COL ? "dst_cols" : "dst_rows",
-               [&] { kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a); });
-}
-template <int K, bool COL>
-void launch_tau_k(fde_handle h, const LineArgs& a) {
-  using C = LaunchCfg<K, COL, 1>;
-  auto kern = k_tau_lines<K, KR, COL, C::FPC>;
-  const int npairs = (a.nlines + 1) / 2;
-  launch_named(h, COL ? "tau_cols" : "tau_rows",
-               [&] { kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a); });
-}
-
 template <int KM, bool COL, bool TAU>
 void launch_dstm_k(fde_handle h, const LineArgs& a) {
   using C = LaunchCfgM<KM, COL>;
-  auto kern = k_dstm_lines<KM, KR, COL, C::FPC, TAU>;
+  auto kern = k_dstm_lines<KM, KRM, COL, C::FPC, TAU>;
   const int npairs = (a.nlines + 1) / 2;
+  const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
   launch_named(h, TAU ? (COL ? "tau_cols" : "tau_rows") : (COL ? "dst_cols" : "dst_rows"),
-               [&] { kern<<<(npairs + C::FPC - 1) / C::FPC, C::THREADS, C::SMEM, h->st>>>(a); });
+               [&] { kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a); });
 }
 
 #define FDE_SWITCH_K(K, CALL)                                           \
@@ -353,22 +348,22 @@ void init_kernel_attrs() {
   set_attr_toep<K, true, true>();
   using D0 = LaunchCfgM<K - 1, false>;
   using D1 = LaunchCfgM<K - 1, true>;
-  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KR, false, D0::FPC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
-  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KR, false, D0::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
-  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KR, true, D1::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D1::SMEM));
-  using C0 = LaunchCfg<K, false, 1>;
-  using C1 = LaunchCfg<K, true, 1>;
+  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, false, D0::FPC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
+  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, false, D0::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
+  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, true, D1::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D1::SMEM));
 }
 
 // One Toeplitz pass along rows (COL=false) or columns (COL=true).
-void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const double* yin, double nu, const int* gate) {
+void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const double* yin, double nu, const int* gate,
+                   const KryFuse* kf = nullptr) {
   LineArgs a = base_args(h);
+  if (kf) a.kf = *kf;
   a.x = x;
   a.y = y;
   a.yin = yin;
   a.nu = nu;
   a.gate = gate;
-  a.nlines = h->dims == 1 ? h->batch : h->batch * h->n;
+  a.nlines = h->dims == 1 ? 1 : h->n;
   const bool var = col ? h->var_y : h->var_x;
   if (!var) {
     a.mu = col ? h->mu_y : h->mu_x;
@@ -395,7 +390,10 @@ void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const dou
   a1.mu = muS;
   a1.omul = a.cP;
   a1.y = y;
+  a1.kf.mode &= ~KM_PQ;     // p = z + βp once (first launch), p·q after the second
   LineArgs a2 = a;
+  a2.kf.mode &= ~KM_PUPD;
+  a2.x = (a.kf.mode & KM_PUPD) ? a.kf.p : x;
   a2.mu = muK;
   a2.omul = a.cM;
   a2.nu = 0.0;
@@ -410,13 +408,24 @@ void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const dou
   }
 }
 
-// y = A x (a1)
-void op_matvec(fde_handle h, const double* x, double* y, const int* gate) {
+// y = A x (a1). With kf (fused PCG): x is z, the row pass forms p = z + βp
+// (KM_PUPD) and the pass completing y = A p accumulates p·y (KM_PQ).
+void op_matvec(fde_handle h, const double* x, double* y, const int* gate, const KryFuse* kf = nullptr) {
+  KryFuse k0{}, k1{};
+  if (kf) {
+    k0 = *kf;
+    k1 = *kf;
+    if (h->dims == 2) {
+      k0.mode &= (KM_PUPD | KM_GATE);
+      k1.mode &= (KM_PQ | KM_GATE);
+    }
+  }
   if (h->dims == 1) {
-    toeplitz_pass(h, false, x, y, nullptr, h->d.nu, gate);
+    toeplitz_pass(h, false, x, y, nullptr, h->d.nu, gate, kf ? &k0 : nullptr);
   } else {
-    toeplitz_pass(h, false, x, h->wx, nullptr, h->d.nu, gate);
-    toeplitz_pass(h, true, x, y, h->wx, 0.0, gate);
+    const double* xc = (kf && (kf->mode & KM_PUPD)) ? kf->p : x;
+    toeplitz_pass(h, false, x, h->wx, nullptr, h->d.nu, gate, kf ? &k0 : nullptr);
+    toeplitz_pass(h, true, xc, y, h->wx, 0.0, gate, kf ? &k1 : nullptr);
   }
 }
 
@@ -425,18 +434,35 @@ void op_copy(fde_handle h, const double* src, double* dst) {
   launch_named(h, "copy", [&] { k_copy<<<592, 256, 0, h->st>>>(src, dst, n); });
 }
 
-// z = P⁻¹ r (a2)
-void op_tau(fde_handle h, const double* r, double* z, const int* gate) {
+// z = P⁻¹ r (a2). With kf (fused PCG): the first kernel forms r -= αq,
+// x += αp (KM_XR, r is read from kf->r) and the last accumulates r·z (KM_RZ).
+void op_tau(fde_handle h, const double* r, double* z, const int* gate, const KryFuse* kf = nullptr) {
+  KryFuse kpre{}, kmid{}, kpost{};
+  if (kf) {
+    kpre = kmid = kpost = *kf;
+    if (h->dims == 2) {
+      kpre.mode &= (KM_XR | KM_GATE);
+      kmid.mode &= KM_GATE;
+      kpost.mode &= (KM_RZ | KM_GATE);
+    }
+  }
   if (h->d.prec == FDE_PREC_NONE) {
-    op_copy(h, r, z);
+    if (kf) {
+      const KryFuse k = *kf;
+      const int N = h->N;
+      launch_named(h, "pcg_xrz_none", [&] { k_pcg_xrz_none<<<dim3(296, h->batch), 256, 0, h->st>>>(k, N, z); });
+    } else {
+      op_copy(h, r, z);
+    }
     return;
   }
   LineArgs a = base_args(h);
   a.gate = gate;
+  if (kf) a.kf = kpre;
   if (h->dims == 1) {
     a.x = r;
     a.y = z;
-    a.nlines = h->batch;
+    a.nlines = 1;
     a.invF = h->invF;
     a.dpre = h->dpre;
     a.dpost = h->dpost;
@@ -444,14 +470,15 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate) {
     return;
   }
   // 2D: rows DST (pre-scale) -> columns DST·F⁻¹·DST -> rows DST (post-scale)
-  a.nlines = h->batch * h->n;
+  a.nlines = h->n;
   a.x = r;
   a.y = h->t1;
   a.dpre = h->dpre;
   FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, a)));
   LineArgs b = base_args(h);
   b.gate = gate;
-  b.nlines = h->batch * h->n;
+  if (kf) b.kf = kmid;
+  b.nlines = h->n;
   b.x = h->t1;
   b.y = h->t2;
   b.Fx = h->Fx;
@@ -460,7 +487,8 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate) {
   FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, true, true>(h, b)));
   LineArgs c = base_args(h);
   c.gate = gate;
-  c.nlines = h->batch * h->n;
+  if (kf) c.kf = kpost;
+  c.nlines = h->n;
   c.x = h->t2;
   c.y = z;
   c.dpost = h->dpost;
@@ -510,7 +538,7 @@ void build(fde_handle h, const fde_desc* d) {
   h->tw = h->upload(tw);
   // per-pass twiddle tables of the length-L (Toeplitz) and length-m (DST) FFTs
   h->twp = h->upload(pass_twiddles_host(h->K, KR));
-  h->twpm = h->upload(pass_twiddles_host(h->K - 1, KR));
+  h->twpm = h->upload(pass_twiddles_host(h->K - 1, KRM));
   {
     std::vector<double> sv(m);
     for (int j = 0; j < m; ++j) sv[j] = std::sin(M_PI * (double)std::min(j, m - j) / (double)m);  // sin(πj/m)
@@ -740,6 +768,7 @@ void ensure_krylov(fde_handle h, int nvecV) {
     h->kz = h->dalloc<double>(ve);
     h->kp = h->dalloc<double>(ve);
     h->kq = h->dalloc<double>(ve);
+    h->kpart = h->dalloc<double>((size_t)h->batch * 3 * KPMAX);
   }
   if (nvecV > h->V_cols) {
     h->V = h->dalloc<double>(ve * nvecV);
@@ -800,17 +829,23 @@ int read_loops(fde_handle h) {
   return loops;
 }
 
-// one PCG iteration (device-gated)
+// One PCG iteration: the vector work rides in the transform
+// kernels (KryFuse), so a 2D iteration is 5 kernels and a 1D one 2.
 void pcg_iteration(fde_handle h, const VecArgs& va) {
-  const int* gate = &h->ctr->active;
-  op_matvec(h, h->kp, h->kq, gate);
-  k_pcg_pq<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kp, h->kq);
-  k_pcg_xr<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kp, h->kq, h->kx, h->kr);
-  op_tau(h, h->kr, h->kz, gate);
-  k_pcg_rz<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kr, h->kz);
-  k_pcg_p<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kz, h->kp);
-  FDE_CUDA(cudaGetLastError());
-  h->launches += 4;
+  KryFuse kf{};
+  kf.p = h->kp;
+  kf.x = h->kx;
+  kf.r = h->kr;
+  kf.q = h->kq;
+  kf.st = h->sst;
+  kf.ctr = h->ctr;
+  kf.part = h->kpart;
+  kf.rtol = va.rtol;
+  kf.maxit = va.maxit;
+  kf.mode = KM_PUPD | KM_PQ | KM_GATE;
+  op_matvec(h, h->kz, h->kq, nullptr, &kf);
+  kf.mode = KM_XR | KM_RZ | KM_GATE;
+  op_tau(h, h->kr, h->kz, nullptr, &kf);
 }
 
 fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int maxit, fde_stats* st) {
@@ -1072,6 +1107,16 @@ const char* fde_status_str(fde_status s) {
 const char* fde_last_error(fde_handle h) { return h ? h->err.c_str() : "NULL handle"; }
 
 int64_t fde_kernel_launches(fde_handle h) { return h ? (int64_t)h->launches : 0; }
+
+#ifdef FDE_PROBES
+// tools/phase_probe.py: copy the probe array out ([8][2048][8] u64) and reset the slot counter
+int32_t fde_debug_probes(void* host, int64_t bytes) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(host, g_probe, bytes) != cudaSuccess) return -1;
+  g_probe_next = 0;
+  return 0;
+}
+#endif
 
 fde_status fde_profile_unit(fde_handle h, const double* x, double* y, double* z, int32_t reps, void* flush,
                             int64_t flush_bytes, int32_t max_kernels, int32_t* count, double* us,

@@ -22,6 +22,24 @@
 
 namespace fde {
 
+// Phase probes for tools/phase_probe.cu (compiled out unless FDE_PROBES is defined):
+// thread 0 of each CTA records %globaltimer at marker i (slot = LineArgs::probe).
+#ifdef FDE_PROBES
+__device__ unsigned long long g_probe[8][2048][8];   // [launch slot][CTA][marker]
+#define FDE_PROBE(i)                                                                          \
+  do {                                                                                        \
+    if (threadIdx.x == 0) {                                                                   \
+      unsigned long long t_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+      if (blockIdx.x < 2048) g_probe[a.probe & 7][blockIdx.x][i] = t_;                       \
+    }                                                                                         \
+  } while (0)
+#else
+#define FDE_PROBE(i) \
+  do {               \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
@@ -199,25 +217,44 @@ template <class G>
 struct PassTw {
   double2 w[G::R];
 };
+#ifndef FDE_TW_POW
+#define FDE_TW_POW 1   // 1: load W^b, W^2b, W^4b, W^8b and form the other powers by products
+#endif
 template <class G, int I>
 __device__ __forceinline__ void load_pass_tw(PassTw<G>& pt, int t, const TwSrc& tw) {
   constexpr int l = G::lo(I), a = G::ka(I);
   if (l == 0) return;
   const double2* tp = tw.gp + tw_pass_offset<G::K, G::k>(I) + (t & ((1 << l) - 1));
+  if (FDE_TW_POW) {
+    // entry q = bitrev_a(2^i) holds W^{b 2^i}: ka loads instead of 2^ka - 1
 #pragma unroll
-  for (int q = 1; q < (1 << a); ++q) pt.w[q] = tp[q << l];
+    for (int i = 0; i < a; ++i) pt.w[1 << i] = tp[bitrev_c(1 << i, a) << l];
+  } else {
+#pragma unroll
+    for (int q = 1; q < (1 << a); ++q) pt.w[q] = tp[q << l];
+  }
 }
 template <class G, int I, int SIGMA>
-__device__ __forceinline__ void pass_twiddles(double2 (&v)[G::R], const PassTw<G>& pt) {
+__device__ __forceinline__ void pass_twiddles(double2 (&v)[G::R], PassTw<G>& pt) {
   constexpr int l = G::lo(I), a = G::ka(I);
   if (l == 0) return;
+  if (FDE_TW_POW) {
+    // W^{b r} = W^{b (r & (r-1))} · W^{b (r & -r)} (depth <= a-1 products from exact values);
+    // v[q] needs W^{b bitrev(q)}
 #pragma unroll
-  for (int q = 1; q < (1 << a); ++q) v[q] = c_mul_tw<SIGMA>(v[q], pt.w[q]);
+    for (int r = 3; r < (1 << a); ++r)
+      if (r & (r - 1)) pt.w[r] = c_mul(pt.w[r & (r - 1)], pt.w[r & (-r)]);
+#pragma unroll
+    for (int q = 1; q < (1 << a); ++q) v[q] = c_mul_tw<SIGMA>(v[q], pt.w[bitrev_c(q, a)]);
+  } else {
+#pragma unroll
+    for (int q = 1; q < (1 << a); ++q) v[q] = c_mul_tw<SIGMA>(v[q], pt.w[q]);
+  }
 }
 
 // DIF pass I on registers (no memory traffic).
 template <class G, int I, int SIGMA, bool HALF_ZERO>
-__device__ __forceinline__ void dif_pass(double2 (&v)[G::R], const PassTw<G>& tw) {
+__device__ __forceinline__ void dif_pass(double2 (&v)[G::R], PassTw<G>& tw) {
   constexpr int a = G::ka(I);
   if (HALF_ZERO && a == G::k) {
     // upper half of the inputs are zero: first radix-2 stage is a copy/twiddle
@@ -243,7 +280,7 @@ __device__ __forceinline__ void dif_pass(double2 (&v)[G::R], const PassTw<G>& tw
 }
 
 template <class G, int I, int SIGMA>
-__device__ __forceinline__ void dit_pass(double2 (&v)[G::R], const PassTw<G>& tw) {
+__device__ __forceinline__ void dit_pass(double2 (&v)[G::R], PassTw<G>& tw) {
   constexpr int a = G::ka(I);
   pass_twiddles<G, I, SIGMA>(v, tw);
   dft_dit<G::k, a, SIGMA>(v);

@@ -165,15 +165,14 @@ __global__ void k_pcg_init(VecArgs a, const double* __restrict__ b, double* __re
   }
 }
 
-// p = z; rho = r·z
+// rho = r·z; p = 0 and β = 0, so that the first fused iteration's p = z + β p = z
 __global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const double* __restrict__ z, double* __restrict__ p) {
   const int rb = blockIdx.y, N = a.N;
   const size_t o = (size_t)rb * N;
   double acc[1] = {0.0};
   FDE_GRID_LOOP(e) {
-    const double zv = z[o + e];
-    p[o + e] = zv;
-    acc[0] = fma(r[o + e], zv, acc[0]);
+    p[o + e] = 0.0;
+    acc[0] = fma(r[o + e], z[o + e], acc[0]);
   }
   __shared__ double red[32];
   block_sum<1>(acc, red);
@@ -185,6 +184,7 @@ __global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const doubl
     if (threadIdx.x == 0) {
       SolveState& s = a.st[rb];
       s.rho = out[0];
+      s.betac = 0.0;
       if (s.cyc_active && !(s.rho > 0.0)) {
         s.status = isfinite(s.rho) ? ST_NOT_SPD : ST_NONFINITE;
         mark_finished(a, s);
@@ -564,6 +564,129 @@ __global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const doub
       }
     }
   }
+}
+
+// ===================================================== fused Krylov work ====
+// PCG vector work carried by the transform kernels (line_kernels.cuh,
+// dst_kernels.cuh) in their prologues/epilogues; LineArgs::kmode is a bitmask:
+//   KM_PUPD  prologue of the row Toeplitz pass:  p = z + β p (written back), FFT input p
+//   KM_PQ    epilogue of the Toeplitz pass that completes q = A p: partial p·q -> α = ρ/(p·q)
+//   KM_XR    prologue of the first τ kernel:  x += α p, r -= α q (written back),
+//            partial ‖r‖² -> iteration count and convergence (R10)
+//   KM_RZ    epilogue of the last τ kernel:   partial r·z -> ρ' , β = ρ'/ρ
+//   KM_GATE  no vector work; CTAs of finished RHS exit
+// Partials: kpart[(rhs*3 + slot)*KPMAX + blockIdx.x]; the last CTA of each RHS
+// (ticket) sums them in fixed order (deterministic) and updates SolveState.
+enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16 };
+constexpr int KPMAX = 4096;   // CTAs per RHS of one line kernel
+
+struct KryFuse {
+  int mode;
+  double* p;
+  double* x;
+  double* r;
+  const double* q;
+  SolveState* st;
+  Counters* ctr;
+  double* part;
+  double rtol;
+  int maxit;
+};
+
+__device__ __forceinline__ void finish_rhs(Counters* c, SolveState& s) {
+  if (s.cyc_active) { s.cyc_active = 0; atomicSub(&c->active, 1); }
+  if (!s.finished) { s.finished = 1; atomicSub(&c->unfinished, 1); }
+}
+
+// CTA-wide reduction of acc[0..2] (slots PQ, RR, RZ used by k.mode), partial
+// store, and the per-RHS finalisation by the last CTA. All threads call it.
+__device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&acc)[3]) {
+  __shared__ double red[3 * 32];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int rhs = blockIdx.y;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double v = warp_sum(acc[i]);
+    if (lane == 0) red[i * 32 + wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[threadIdx.x * 32 + w];
+    k.part[((size_t)rhs * 3 + threadIdx.x) * KPMAX + blockIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned tk = atomicAdd(&k.ctr->tickets[rhs * 8 + 1], 1u);
+    s_last = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  __shared__ double tot[3];
+  for (int i = wid; i < 3; i += nw) {  // one warp per slot (blocks may have < 3 warps)
+    double s = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(k.part + ((size_t)rhs * 3 + i) * KPMAX + b);
+    s = warp_sum(s);
+    if (lane == 0) tot[i] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  k.ctr->tickets[rhs * 8 + 1] = 0u;
+  SolveState& s = k.st[rhs];
+  if (k.mode & KM_PQ) {
+    const double pq = tot[0];
+    if (!(pq > 0.0)) {
+      s.status = isfinite(pq) ? ST_NOT_SPD : ST_NONFINITE;
+      finish_rhs(k.ctr, s);
+    } else {
+      s.alpha = s.rho / pq;
+    }
+  }
+  if (k.mode & KM_XR) {
+    const double rn = sqrt(tot[1]);
+    s.iters += 1;
+    s.rnorm = rn / s.bnorm;
+    if (!isfinite(rn)) {
+      s.status = ST_NONFINITE;
+      finish_rhs(k.ctr, s);
+    } else if (rn <= k.rtol * s.bnorm) {
+      s.converged = 1;
+      finish_rhs(k.ctr, s);
+    } else if (s.iters >= k.maxit) {
+      finish_rhs(k.ctr, s);
+    }
+  }
+  if ((k.mode & KM_RZ) && s.cyc_active) {
+    const double rz = tot[2];
+    if (!(rz > 0.0)) {
+      s.status = isfinite(rz) ? ST_NOT_SPD : ST_NONFINITE;
+      finish_rhs(k.ctr, s);
+    } else {
+      s.betac = rz / s.rho;
+      s.rho = rz;
+    }
+  }
+}
+
+// PREC_NONE τ step of the fused PCG: x += α p, r -= α q, z = r (‖r‖² and r·z partials)
+__global__ void k_pcg_xrz_none(KryFuse k, int N, double* __restrict__ z) {
+  const int rhs = blockIdx.y;
+  if (!k.st[rhs].cyc_active) return;
+  const double al = k.st[rhs].alpha;
+  const size_t o = (size_t)rhs * N;
+  double acc[3] = {0.0, 0.0, 0.0};
+  FDE_GRID_LOOP(e) {
+    const double rv = fma(-al, k.q[o + e], k.r[o + e]);
+    k.r[o + e] = rv;
+    k.x[o + e] = fma(al, k.p[o + e], k.x[o + e]);
+    z[o + e] = rv;
+    acc[1] = fma(rv, rv, acc[1]);
+  }
+  acc[2] = acc[1];
+  kry_reduce_finalize(k, acc);
 }
 
 // while-loop control of a CUDA graph (conditional WHILE node): keep looping

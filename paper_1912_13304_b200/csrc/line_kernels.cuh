@@ -14,6 +14,7 @@
 // transform kernels.
 #pragma once
 #include "fft_engine.cuh"
+#include "krylov_kernels.cuh"
 
 namespace fde {
 
@@ -22,7 +23,7 @@ struct LineArgs {
   double* y;              // output lines
   const double* yin;      // optional partial added to the output (column pass) or nullptr
   int n;                  // points per line
-  int nlines;             // number of lines (rows: batch*n_rows, cols: batch*n)
+  int nlines;             // lines per RHS (rows: N/n, cols: n); the RHS is blockIdx.y
   int N;                  // elements per RHS (n or n*n)
   double nu;              // shift ν·x added to the output (0 to skip)
   const double2* tw;      // quarter twiddle table exp(-2 pi i r/L), r < L/4 (FDE_TW_MODE 0)
@@ -42,33 +43,43 @@ struct LineArgs {
   const double* Fx;       // 2D τ (columns): cx·F_α(θ_i), i = 0..n-1
   const double* Fy;       // 2D τ (columns): cy·F_β(θ_j), j = 0..n-1
   double fscale;          // 2D τ: multiplier scale folded with 1/F
+  int probe;              // phase-probe slot (FDE_PROBES builds only)
+  KryFuse kf;             // fused PCG vector work (krylov_kernels.cuh); kf.mode = 0: none
 };
 
+// per-RHS gate of the fused Krylov kernels: CTAs of a finished RHS exit at once
+__device__ __forceinline__ bool kry_skip(const LineArgs& a) {
+  return a.kf.mode != 0 && !a.kf.st[blockIdx.y].cyc_active;
+}
+
 // line addressing ----------------------------------------------------------
-// Element p of line l is at base + p*stride; its coefficient-field index is
-// fbase + p*stride (fields are shared by all RHS).
-//   rows: l = b*rows + r  -> base = l*n, stride 1, fbase = r*n
-//   cols: l = b*n + c     -> base = b*N + c, stride n, fbase = c
+// Kernels run on a grid (pairs of lines / FPC, batch): blockIdx.y is the RHS,
+// lines are numbered within one RHS, so a line pair never straddles two RHS
+// (the fused Krylov reductions are per RHS). Element p of line l of RHS b is
+// at base + p*stride; its coefficient-field index (fields are shared by all
+// RHS) is fbase + p*stride.
+//   rows: l < N/n  -> base = b*N + l*n, stride 1, fbase = l*n
+//   cols: l < n    -> base = b*N + l,   stride n, fbase = l
 struct Line {
   long long base;
   int stride, fbase;
 };
 template <bool COL>
-__device__ __forceinline__ Line line_of(int l, int n, int N) {
+__device__ __forceinline__ Line line_of(int l, int b, int n, int N) {
   Line L;
-  if (!COL) {
-    const int rows = N / n;
-    L.base = (long long)l * n;
-    L.stride = 1;
-    L.fbase = (l % rows) * n;
-  } else {
-    const int b = l / n, c = l - b * n;
-    L.base = (long long)b * N + c;
-    L.stride = n;
-    L.fbase = c;
-  }
+  L.base = (long long)b * N + (COL ? l : (long long)l * n);
+  L.stride = COL ? n : 1;
+  L.fbase = COL ? l : l * n;
   return L;
 }
+
+// 8-byte asynchronous global -> shared copy (LDGSTS): the copy proceeds while
+// the thread computes; cp_async_wait_all() before reading the destination.
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // 1/x to ~1 ulp for 1e-30 < x < 1e30: fp32 seed + two Newton steps (FP64 FMA),
 // avoiding the IEEE division slow path inside the transform kernels.
@@ -104,37 +115,62 @@ k_toeplitz_lines(LineArgs a) {
   using M = LineMap<G, COL, FPC>;
   extern __shared__ double2 smem_all[];
   if (a.gate && *a.gate == 0) return;
+  if (kry_skip(a)) return;
   double2* sm_tw = smem_all;
   double2* smem = smem_all + TW_SMEM_QUARTER * (G::L >> 2);
   const TwSrc tws{sm_tw, a.twp};
   const int f = M::group(), t = M::lane();
   double2* sm = smem + (size_t)f * G::SM_STRIDE * (VAR ? 2 : 1);
   double2* smZ = sm + G::SM_STRIDE;
+  // column pass: the other direction's partial (yin) streams into shared memory
+  // while the transform runs (one slot per epilogue position of this thread)
+  double2* smY = smem + (size_t)FPC * G::SM_STRIDE * (VAR ? 2 : 1) + (size_t)f * (G::L / 2);
+  FDE_PROBE(0);
   const int g = blockIdx.x * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
   const int n = a.n;
-  const Line A0 = line_of<COL>(v0 ? l0 : 0, n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, n, a.N);
+  const Line A0 = line_of<COL>(v0 ? l0 : 0, blockIdx.y, n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, blockIdx.y, n, a.N);
 
   double2 v[G::R];
+  const bool pupd = (a.kf.mode & KM_PUPD) != 0;
+  const double beta = pupd ? a.kf.st[blockIdx.y].betac : 0.0;
 #pragma unroll
   for (int q = 0; q < G::R / 2; ++q) {
     const int p = (q << (K - k)) | t;
     double re = 0.0, im = 0.0;
     if (p < n) {
-      if (v0) re = __ldg(a.x + A0.base + (long long)p * A0.stride);
-      if (v1) im = __ldg(a.x + A1.base + (long long)p * A1.stride);
+      const long long o0 = A0.base + (long long)p * A0.stride, o1 = A1.base + (long long)p * A1.stride;
+      if (v0) re = __ldg(a.x + o0);
+      if (v1) im = __ldg(a.x + o1);
+      if (pupd) {  // p = z + β p (KM_PUPD; a.x = z)
+        if (v0) { re = fma(beta, a.kf.p[o0], re); a.kf.p[o0] = re; }
+        if (v1) { im = fma(beta, a.kf.p[o1], im); a.kf.p[o1] = im; }
+      }
     }
     v[q] = make_double2(re, im);
   }
 #pragma unroll
   for (int q = G::R / 2; q < G::R; ++q) v[q] = make_double2(0.0, 0.0);
+  if (COL && a.yin) {
+#pragma unroll
+    for (int q = 0; q < G::R / 2; ++q) {
+      const int p = (q << (K - k)) | t;
+      if (p < n) {
+        if (v0) cp_async8(&smY[p].x, a.yin + A0.base + (long long)p * A0.stride);
+        if (v1) cp_async8(&smY[p].y, a.yin + A1.base + (long long)p * A1.stride);
+      }
+    }
+  }
   if (TW_SMEM_QUARTER) {
     load_twiddles(sm_tw, a.tw, G::L);
     __syncthreads();
   }
 
+  __syncwarp();
+  FDE_PROBE(1);
   dif_chain<G, -1, true>(v, sm, t, tws);
+  FDE_PROBE(2);
 
   double2 u[G::R / 2];
   if (!VAR) {
@@ -161,6 +197,10 @@ k_toeplitz_lines(LineArgs a) {
     }
     dit_chain<G, +1>(v, sm, t, tws);
   }
+  FDE_PROBE(3);
+  if (COL && a.yin) cp_async_wait_all();
+  double acc[3] = {0.0, 0.0, 0.0};
+  const bool pq = (a.kf.mode & KM_PQ) != 0;
 
 #pragma unroll
   for (int q = 0; q < G::R / 2; ++q) {
@@ -185,39 +225,19 @@ k_toeplitz_lines(LineArgs a) {
     // plain loads (not hoisted above the transform by the compiler)
     if (v0) {
       if (a.nu != 0.0) r0 = fma(a.nu, a.x[o0], r0);
-      if (a.yin) r0 += a.yin[o0];
+      if (a.yin) r0 += COL ? smY[p].x : a.yin[o0];
       a.y[o0] = r0;
+      if (pq) acc[0] = fma(a.kf.p[o0], r0, acc[0]);
     }
     if (v1) {
       if (a.nu != 0.0) r1 = fma(a.nu, a.x[o1], r1);
-      if (a.yin) r1 += a.yin[o1];
+      if (a.yin) r1 += COL ? smY[p].y : a.yin[o1];
       a.y[o1] = r1;
+      if (pq) acc[0] = fma(a.kf.p[o1], r1, acc[0]);
     }
   }
-}
-
-// odd-extension loader: position p of the length-L odd extension of a line
-// (u_0 = u_m = 0, u_j = y_j, u_{L-j} = -y_j, j = 1..n; y_j is element j-1)
-__device__ __forceinline__ double2 load_oddext(const LineArgs& a, const Line& A0, const Line& A1, bool v0, bool v1,
-                                               int p, int m) {
-  int j = p;
-  double sgn = 1.0;
-  if (p > m) { j = 2 * m - p; sgn = -1.0; }
-  double re = 0.0, im = 0.0;
-  if (j >= 1 && j < m) {
-    const int e = j - 1;
-    if (v0) {
-      double val = __ldg(a.x + A0.base + (long long)e * A0.stride);
-      if (a.dpre) val *= __ldg(a.dpre + A0.fbase + e * A0.stride);
-      re = sgn * val;
-    }
-    if (v1) {
-      double val = __ldg(a.x + A1.base + (long long)e * A1.stride);
-      if (a.dpre) val *= __ldg(a.dpre + A1.fbase + e * A1.stride);
-      im = sgn * val;
-    }
-  }
-  return make_double2(re, im);
+  FDE_PROBE(4);
+  if (pq) kry_reduce_finalize(a.kf, acc);
 }
 
 __device__ __forceinline__ void store_pair(const LineArgs& a, const Line& A0, const Line& A1, bool v0, bool v1, int e,
@@ -229,128 +249,6 @@ __device__ __forceinline__ void store_pair(const LineArgs& a, const Line& A0, co
   if (v1) {
     if (a.dpost) r1 *= __ldg(a.dpost + A1.fbase + e * A1.stride);
     a.y[A1.base + (long long)e * A1.stride] = r1;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Raw DST-I along lines: out_k = sqrt(2m)·(S_n (dpre ⊙ y))_k (normalisation is
-// folded into the τ multiplier), optional post-scale dpost.
-// ---------------------------------------------------------------------------
-template <int K, int k, bool COL, int FPC>
-__global__ void __launch_bounds__(FPC * (1 << (K - k)), min_blocks_for(FPC * (1 << (K - k))))
-k_dst_lines(LineArgs a) {
-  using G = FftGeom<K, k>;
-  using M = LineMap<G, COL, FPC>;
-  extern __shared__ double2 smem_all[];
-  if (a.gate && *a.gate == 0) return;
-  double2* sm_tw = smem_all;
-  double2* smem = smem_all + TW_SMEM_QUARTER * (G::L >> 2);
-  const TwSrc tws{sm_tw, a.twp};
-  const int f = M::group(), t = M::lane();
-  double2* sm = smem + (size_t)f * G::SM_STRIDE;
-  const int g = blockIdx.x * FPC + f;
-  const int l0 = 2 * g, l1 = 2 * g + 1;
-  const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
-  const Line A0 = line_of<COL>(v0 ? l0 : 0, a.n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, a.n, a.N);
-  constexpr int m = G::L / 2;
-
-  double2 v[G::R];
-#pragma unroll
-  for (int q = 0; q < G::R; ++q) v[q] = load_oddext(a, A0, A1, v0, v1, (q << (K - k)) | t, m);
-  if (TW_SMEM_QUARTER) {
-    load_twiddles(sm_tw, a.tw, G::L);
-    __syncthreads();
-  }
-
-  dif_chain<G, -1, false>(v, sm, t, tws);
-  // permute bit-reversed -> natural through shared memory
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < G::R; ++q) {
-    const int fr = bitrev_dev((t << k) | q, K);
-    if (fr >= 1 && fr < m) sm[G::phys(fr)] = v[q];
-  }
-  __syncthreads();
-  // natural order: frequency fr = 1..n -> element fr-1; thread t covers fr = t + 1 + P*i
-#pragma unroll
-  for (int i = 0; i < G::R / 2; ++i) {
-    const int fr = 1 + t + G::P * i;
-    if (fr >= m) continue;
-    const double2 U = sm[G::phys(fr)];
-    store_pair(a, A0, A1, v0, v1, fr - 1, -U.y, U.x);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// DST -> ×(1/F) -> DST along lines (the τ-solve core):
-//   1D (rows, !COL):  z = dpost ⊙ S(invF ⊙ S(dpre ⊙ r))
-//   2D (cols, COL):   the y-direction part of (S⊗S)F⁻¹(S⊗S) on data already
-//                     sine-transformed along x; F(i,j) = Fx[i] + Fy[j].
-// With U = DFT(oddext(r1 + i r2)), V = U ⊙ (i·invF_ext·scale) is itself the
-// odd extension of the scaled sine coefficients, so a second forward DFT
-// finishes the job.
-// ---------------------------------------------------------------------------
-template <int K, int k, bool COL, int FPC>
-__global__ void __launch_bounds__(FPC * (1 << (K - k)), min_blocks_for(FPC * (1 << (K - k))))
-k_tau_lines(LineArgs a) {
-  using G = FftGeom<K, k>;
-  using M = LineMap<G, COL, FPC>;
-  extern __shared__ double2 smem_all[];
-  if (a.gate && *a.gate == 0) return;
-  double2* sm_tw = smem_all;
-  double2* smem = smem_all + TW_SMEM_QUARTER * (G::L >> 2);
-  const TwSrc tws{sm_tw, a.twp};
-  const int f = M::group(), t = M::lane();
-  double2* sm = smem + (size_t)f * G::SM_STRIDE;
-  const int g = blockIdx.x * FPC + f;
-  const int l0 = 2 * g, l1 = 2 * g + 1;
-  const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
-  const Line A0 = line_of<COL>(v0 ? l0 : 0, a.n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, a.n, a.N);
-  constexpr int m = G::L / 2;
-
-  double2 v[G::R];
-#pragma unroll
-  for (int q = 0; q < G::R; ++q) v[q] = load_oddext(a, A0, A1, v0, v1, (q << (K - k)) | t, m);
-  if (TW_SMEM_QUARTER) {
-    load_twiddles(sm_tw, a.tw, G::L);
-    __syncthreads();
-  }
-
-  dif_chain<G, -1, false>(v, sm, t, tws);
-
-  // x-frequency of this column pair (2D): both lines of a pair are columns c, c+1
-  const double fx0 = COL ? __ldg(a.Fx + A0.fbase) : 0.0;
-  const double fx1 = COL ? __ldg(a.Fx + (v1 ? A1.fbase : A0.fbase)) : 0.0;
-#pragma unroll
-  for (int q = 0; q < G::R; ++q) {
-    const int fr = bitrev_dev((t << k) | q, K);
-    const int j = fr <= m ? fr : G::L - fr;  // even extension index
-    double s0 = 0.0, s1 = 0.0;
-    if (j >= 1 && j < m) {
-      if (!COL) {
-        s0 = s1 = a.invF[j - 1];
-      } else {
-        const double fy = a.Fy[j - 1];
-        s0 = a.fscale * fast_rcp(fx0 + fy);
-        s1 = a.fscale * fast_rcp(fx1 + fy);
-      }
-    }
-    // packed pair U = DFT(oddext(r0 + i r1)): line 0's sine coefficients sit in
-    // -Im U, line 1's in Re U; V = (-s0·U.y) + i(s1·U.x) is the odd extension
-    // of the scaled coefficients of both lines, packed the same way.
-    const double2 U = v[q];
-    v[q] = make_double2(-s0 * U.y, s1 * U.x);
-  }
-  // second forward DFT from bit-reversed input (DIT, sigma = -1)
-  __syncthreads();
-  dit_chain<G, -1>(v, sm, t, tws);
-
-#pragma unroll
-  for (int q = 0; q < G::R / 2; ++q) {
-    const int p = (q << (K - k)) | t;
-    if (p < 1 || p >= m) continue;
-    const double2 W = v[q];
-    store_pair(a, A0, A1, v0, v1, p - 1, -W.y, W.x);
   }
 }
 
