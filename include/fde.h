@@ -145,6 +145,18 @@ fde_status fde_profile_unit(fde_handle h, const double* x, double* y, double* z,
                             int64_t flush_bytes, int32_t max_kernels, int32_t* count, double* us,
                             const char** names);
 
+/* Measurement support: run a solve (solver 0 = fde_pcg, 1 = fde_gmres right-
+ * preconditioned with `restart`) for at most `maxit` iterations, then run ONE
+ * more loop body (a PCG iteration / a GMRES cycle) on that mid-solve state
+ * kernel by kernel, each launch bracketed by CUDA events on the handle's
+ * stream (warm L2, the kernels and launch configuration the solvers use).
+ * On return us[i] is the device time (µs) of the i-th kernel of that body,
+ * names[i] its static name, *count the kernels per body; x and st hold the
+ * stopped solve's result (status FDE_ERR_NOT_CONVERGED if maxit was hit). */
+fde_status fde_profile_solve(fde_handle h, const double* b, double* x, double rtol, int32_t maxit, int32_t solver,
+                             int32_t restart, int32_t max_kernels, int32_t* count, double* us, const char** names,
+                             fde_stats* st);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -21,7 +22,7 @@
 #include "../../include/fde.h"
 #include "krylov_kernels.cuh"
 #include "line_kernels.cuh"
-#include "dst_kernels.cuh"
+#include "sine_kernels.cuh"
 
 using namespace fde;
 
@@ -190,6 +191,25 @@ struct LaunchCfgM {
   static constexpr int SMEM = FPC * SPG + SCR;
 };
 
+// sine-domain operator kernels (sine_kernels.cuh)
+template <int KM, bool COL, int MODE>
+struct LaunchCfgS {
+  using GT = FftGeom<KM + 1, 4>;
+  static constexpr int P = 1 << (KM - 3);
+  static constexpr int SPG = GT::SM_STRIDE * 16 + (MODE == 1 ? FftGeom<KM, 3>::SM_STRIDE * 16 : 0);
+  static constexpr int BY_SMEM = (200 * 1024) / SPG > 0 ? (200 * 1024) / SPG : 1;
+  static constexpr int BY_THR = 512 / P > 0 ? 512 / P : 1;
+#ifndef FDE_SINE_COL_FPC
+#define FDE_SINE_COL_FPC 2
+#endif
+  static constexpr int WANT = COL ? (128 / P > FDE_SINE_COL_FPC ? 128 / P : FDE_SINE_COL_FPC) : (128 / P > 1 ? 128 / P : 1);
+  static constexpr int FPC0 = WANT < BY_THR ? WANT : BY_THR;
+  static constexpr int FPC = FPC0 < BY_SMEM ? FPC0 : BY_SMEM;
+  static constexpr int THREADS = FPC * P;
+  static constexpr int SCR = (FPC * (GroupScan<COL, P, FPC>::NSEG + 1) * 2) * 8;
+  static constexpr int SMEM = FPC * SPG + SCR;
+};
+
 }  // namespace
 
 // ======================================================================== handle
@@ -207,6 +227,7 @@ struct fde_handle_s {
   double2* twpm = nullptr;
   double* sinm = nullptr;
   double2 *mu_x = nullptr, *mu_y = nullptr;
+  double2 *mus_x = nullptr, *mus_y = nullptr;  // sine-domain μ_s (constant directions; sine_kernels.cuh)
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
   double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
   double *invF = nullptr, *Fx = nullptr, *Fy = nullptr;
@@ -233,6 +254,8 @@ struct fde_handle_s {
   double g_rtol = -1.0;
   int g_maxit = -1;
 
+  bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
+  bool no_graph = false;            // env FDE_GRAPH=0: host-driven loop (for profilers)
   std::vector<void*> allocs;
   // profiling (fde_profile_unit)
   bool prof = false;
@@ -317,6 +340,21 @@ void launch_dstm_k(fde_handle h, const LineArgs& a) {
                [&] { kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a); });
 }
 
+template <int KM, bool COL, int MODE>
+void launch_sineop_k(fde_handle h, const LineArgs& a) {
+  using C = LaunchCfgS<KM, COL, MODE>;
+  auto kern = k_sineop_lines<KM, COL, C::FPC, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    FDE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  const int npairs = (a.nlines + 1) / 2;
+  const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
+  launch_named(h, MODE == 0 ? "sine_op_rows" : (MODE == 1 ? "sine_op_cols" : "sine_op_1d"),
+               [&] { kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a); });
+}
+
 #define FDE_SWITCH_K(K, CALL)                                           \
   switch (K) {                                                          \
     case 6: { constexpr int KK = 6; CALL; } break;                      \
@@ -351,6 +389,7 @@ void init_kernel_attrs() {
   FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, false, D0::FPC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
   FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, false, D0::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
   FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, true, D1::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D1::SMEM));
+  FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, true, D1::FPC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, D1::SMEM));
 }
 
 // One Toeplitz pass along rows (COL=false) or columns (COL=true).
@@ -554,7 +593,8 @@ void build(fde_handle h, const fde_desc* d) {
     host_fft(c);
     return c;
   };
-  auto make_dir = [&](double order, bool var, double cpl, double cmi, double wgt, double shift, double2*& mu, double*& lS,
+  auto make_dir = [&](double order, bool var, double cpl, double cmi, double wgt, double shift, double2*& mu, double2*& mus,
+                      double*& lS,
                       double*& lK, double*& cPf, double*& cMf, const std::vector<double>& fp,
                       const std::vector<double>& fm) {
     std::vector<std::complex<double>> lam = lambda(order);
@@ -568,6 +608,14 @@ void build(fde_handle h, const fde_desc* d) {
         mv[s] = make_double2((shift + wgt * (cpl + cmi) * l.real()) * invL, wgt * (cpl - cmi) * l.imag() * invL);
       }
       mu = h->upload(mv);
+      // sine domain: D T D / (2m) = S T S with D = sqrt(2m) S; no ν (applied once, per element)
+      std::vector<double2> ms(L);
+      const double s2m = 1.0 / (2.0 * m);
+      for (int s = 0; s < L; ++s) {
+        const std::complex<double> l = lam[bitrev_host(s, h->K)];
+        ms[s] = make_double2(wgt * (cpl + cmi) * l.real() * invL * s2m, wgt * (cpl - cmi) * l.imag() * invL * s2m);
+      }
+      mus = h->upload(ms);
     } else {
       std::vector<double> s1(L), s2(L);
       std::vector<double2> mv(2 * L);  // two-pass fallback multipliers
@@ -587,8 +635,8 @@ void build(fde_handle h, const fde_desc* d) {
       cMf = h->upload(q);
     }
   };
-  make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, d->nu, h->mu_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm);
-  if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, 0.0, h->mu_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em);
+  make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, d->nu, h->mu_x, h->mus_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm);
+  if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, 0.0, h->mu_y, h->mus_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em);
 
   // preconditioner tables
   const int prec = d->prec;
@@ -623,6 +671,9 @@ void build(fde_handle h, const fde_desc* d) {
       std::vector<double> inv(n);
       for (int j = 0; j < n; ++j) inv[j] = 1.0 / (cx * Fa[j]) / (2.0 * m);
       h->invF = h->upload(inv);
+      std::vector<double> fx(n);
+      for (int j = 0; j < n; ++j) fx[j] = cx * Fa[j];
+      h->Fx = h->upload(fx);  // unscaled samples for the sine-domain PCG
     } else {
       for (int j = 0; j < n; ++j) { Fa[j] *= cx; Fb[j] *= cy; }
       h->Fx = h->upload(Fa);
@@ -657,6 +708,12 @@ void build(fde_handle h, const fde_desc* d) {
   h->sst = h->dalloc<SolveState>(h->batch);
   h->gsm = h->dalloc<GmresSmall>(h->batch);
   h->ctr = h->dalloc<Counters>(1);
+  {
+    const char* e = std::getenv("FDE_PCG");
+    h->force_standard_pcg = e && std::strcmp(e, "standard") == 0;
+    const char* g = std::getenv("FDE_GRAPH");
+    h->no_graph = g && std::strcmp(g, "0") == 0;
+  }
   h->part = h->dalloc<double>((size_t)h->batch * (MAX_RESTART + 1) * RED_BLOCKS);
   FDE_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->st));
   FDE_CUDA(cudaMemsetAsync(h->sst, 0, sizeof(SolveState) * h->batch, h->st));
@@ -759,6 +816,20 @@ __global__ void k_reset_counters(Counters* c, SolveState* s, int batch) {
   }
 }
 
+// measurement: every RHS iterating again (fde_profile_solve)
+__global__ void k_reactivate(Counters* c, SolveState* s, int batch) {
+  if (threadIdx.x == 0) {
+    c->active = batch;
+    c->unfinished = batch;
+  }
+  if ((int)threadIdx.x < batch) {
+    s[threadIdx.x].cyc_active = 1;
+    s[threadIdx.x].finished = 0;
+    s[threadIdx.x].converged = 0;
+    s[threadIdx.x].status = 0;
+  }
+}
+
 void ensure_krylov(fde_handle h, int nvecV) {
   const size_t ve = h->vec_elems();
   if (!h->kx) {
@@ -823,6 +894,13 @@ int build_while_graph(fde_handle h, cudaGraphExec_t* out, int maxloops, F&& body
   return nodes;
 }
 
+int read_active(fde_handle h) {
+  int v = 0;
+  FDE_CUDA(cudaStreamSynchronize(h->st));
+  FDE_CUDA(cudaMemcpy(&v, &h->ctr->active, sizeof(int), cudaMemcpyDeviceToHost));
+  return v;
+}
+
 int read_loops(fde_handle h) {
   int loops = 0;
   FDE_CUDA(cudaMemcpy(&loops, &h->ctr->loops, sizeof(int), cudaMemcpyDeviceToHost));
@@ -848,7 +926,129 @@ void pcg_iteration(fde_handle h, const VecArgs& va) {
   op_tau(h, h->kr, h->kz, nullptr, &kf);
 }
 
+// ---------------------------------------------------------- sine-domain PCG
+// Constant coefficients with the τ preconditioner: PCG on x̂ = (S⊗S)x
+// (sine_kernels.cuh). Per iteration: 2D = row operator, column operator (+p·q),
+// vector step; 1D = operator, vector step.
+bool sine_pcg_ok(fde_handle h) { return h->d.prec == FDE_PREC_TAU && !h->var_x && !h->var_y; }
+
+KryFuse make_kf(fde_handle h, double rtol, int maxit) {
+  KryFuse kf{};
+  kf.p = h->kp;
+  kf.x = h->kx;
+  kf.r = h->kr;
+  kf.q = h->kq;
+  kf.st = h->sst;
+  kf.ctr = h->ctr;
+  kf.part = h->kpart;
+  kf.rtol = rtol;
+  kf.maxit = maxit;
+  return kf;
+}
+
+// unnormalised 2D (1D) DST of x into y (D⊗D or D, D = sqrt(2m) S), times oscale
+void op_dst_all(fde_handle h, const double* x, double* y, double oscale) {
+  LineArgs a = base_args(h);
+  if (h->dims == 1) {
+    a.nlines = 1;
+    a.x = x;
+    a.y = y;
+    a.oscale = oscale;
+    FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, a)));
+    return;
+  }
+  a.nlines = h->n;
+  a.x = x;
+  a.y = h->t1;
+  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, a)));
+  LineArgs b = base_args(h);
+  b.nlines = h->n;
+  b.x = h->t1;
+  b.y = y;
+  b.oscale = oscale;
+  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, true, false>(h, b)));
+}
+
+void sine_iteration(fde_handle h, double rtol, int maxit) {
+  KryFuse kf = make_kf(h, rtol, maxit);
+  LineArgs a = base_args(h);
+  a.Fx = h->Fx;
+  a.Fy = h->dims == 2 ? h->Fy : nullptr;
+  a.mu = h->mus_x;
+  if (h->dims == 2) {
+    a.nlines = h->n;
+    a.x = h->kr;
+    a.y = h->wx;
+    a.kf = kf;
+    a.kf.mode = KM_PUPD | KM_GATE;
+    FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 0>(h, a)));
+    LineArgs b = base_args(h);
+    b.nlines = h->n;
+    b.x = h->kp;
+    b.yin = h->wx;
+    b.y = h->kq;
+    b.mu = h->mus_y;
+    b.nu = h->d.nu;
+    b.kf = kf;
+    b.kf.mode = KM_PQ | KM_GATE;
+    FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, true, 1>(h, b)));
+  } else {
+    a.nlines = 1;
+    a.x = h->kr;
+    a.y = h->kq;
+    a.nu = h->d.nu;
+    a.kf = kf;
+    a.kf.mode = KM_PUPD | KM_PQ | KM_GATE;
+    FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 2>(h, a)));
+  }
+  KryFuse kv = kf;
+  kv.mode = KM_XR | KM_RZ | KM_GATE;
+  const double* Fx = h->Fx;
+  const double* Fy = h->dims == 2 ? h->Fy : nullptr;
+  const int n = h->n, dims = h->dims;
+  const int gx = dims == 2 ? std::min(n, KPMAX) : 64;
+  launch_named(h, "sine_xr", [&] { k_sine_xr<<<dim3(gx, h->batch), 256, 0, h->st>>>(kv, n, dims, Fx, Fy); });
+}
+
+fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, int maxit, fde_stats* st) {
+  ensure_krylov(h, 0);
+  bool bh = false;
+  const double* bd = stage_in(h, b, h->hin, bh);
+  k_reset_counters<<<1, 32, 0, h->st>>>(h->ctr, h->sst, h->batch);
+  h->launches++;
+  op_dst_all(h, bd, h->kr, 0.0);  // r̂ = b̂ (unnormalised)
+  KryFuse kf = make_kf(h, rtol, maxit);
+  const double* Fx = h->Fx;
+  const double* Fy = h->dims == 2 ? h->Fy : nullptr;
+  const int n = h->n, dims = h->dims;
+  const int gx = dims == 2 ? std::min(n, KPMAX) : 64;
+  launch_named(h, "sine_init", [&] { k_sine_init<<<dim3(gx, h->batch), 256, 0, h->st>>>(kf, n, dims, Fx, Fy); });
+  if (!h->no_graph && (!h->g_pcg || h->g_rtol != rtol || h->g_maxit != maxit)) {
+    if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
+    h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { sine_iteration(h, rtol, maxit); });
+    h->g_rtol = rtol;
+    h->g_maxit = maxit;
+  }
+  if (h->no_graph) {  // FDE_GRAPH=0 (profilers): the same loop body from the host
+    for (int it = 0; it <= maxit; ++it) {
+      sine_iteration(h, rtol, maxit);
+      if ((it & 7) == 7 && read_active(h) == 0) break;
+    }
+  } else {
+    FDE_CUDA(cudaGraphLaunch(h->g_pcg, h->st));
+  }
+  // x = (S⊗S) x̂ = (D⊗D) x̃ / (2m)^dims
+  const double s = 1.0 / (2.0 * h->m);
+  const bool xdev = is_device_ptr(x);
+  op_dst_all(h, h->kx, xdev ? x : h->hout, h->dims == 2 ? s * s : s);
+  if (!xdev) FDE_CUDA(cudaMemcpyAsync(x, h->hout, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  const fde_status ws = worst_status(h, st, true);
+  if (!h->no_graph) h->launches += (long long)read_loops(h) * h->g_pcg_nodes;
+  return ws;
+}
+
 fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int maxit, fde_stats* st) {
+  if (sine_pcg_ok(h) && !h->force_standard_pcg) return run_pcg_sine(h, b, x, rtol, maxit, st);
   ensure_krylov(h, 0);
   bool bh = false;
   const double* bd = stage_in(h, b, h->hin, bh);
@@ -1117,6 +1317,60 @@ int32_t fde_debug_probes(void* host, int64_t bytes) {
   return 0;
 }
 #endif
+
+fde_status fde_profile_solve(fde_handle h, const double* b, double* x, double rtol, int32_t maxit, int32_t solver,
+                             int32_t restart, int32_t max_kernels, int32_t* count, double* us, const char** names,
+                             fde_stats* st) {
+  if (!h) return FDE_ERR_INVALID_ARG;
+  if (!b || !x || !count || !us || !names || max_kernels < 1 || maxit < 1 || (solver != 0 && solver != 1) ||
+      (solver == 1 && (restart < 1 || restart > MAX_RESTART))) {
+    h->err = "fde_profile_solve: bad arguments";
+    return FDE_ERR_INVALID_ARG;
+  }
+  try {
+    // 1. a real solve, stopped after `maxit` iterations (mid-solve state)
+    fde_status rs = solver == 0 ? fde_pcg(h, b, x, rtol, maxit, st) : fde_gmres(h, b, x, rtol, restart, maxit, 0, st);
+    if (rs != FDE_OK && rs != FDE_ERR_NOT_CONVERGED) return rs;
+    // 2. re-activate every RHS and run one more loop body (PCG iteration / GMRES
+    //    cycle) kernel by kernel, each bracketed by CUDA events, no flush
+    k_reactivate<<<1, 32, 0, h->st>>>(h->ctr, h->sst, h->batch);
+    FDE_CUDA(cudaGetLastError());
+    h->flush = nullptr;
+    h->flush_bytes = 0;
+    h->recs.clear();
+    h->prof = true;
+    try {
+      if (solver == 0) {
+        if (sine_pcg_ok(h) && !h->force_standard_pcg) sine_iteration(h, rtol, 1 << 30);
+        else pcg_iteration(h, vec_args(h, rtol, 1 << 30, 0, 0));
+      } else {
+        gmres_cycle(h, vec_args(h, rtol, 1 << 30, restart, 0), restart, 0);
+      }
+    } catch (...) {
+      h->prof = false;
+      throw;
+    }
+    h->prof = false;
+    FDE_CUDA(cudaStreamSynchronize(h->st));
+    const int nk = (int)h->recs.size();
+    *count = nk;
+    for (int i = 0; i < nk && i < max_kernels; ++i) {
+      float ms = 0.f;
+      FDE_CUDA(cudaEventElapsedTime(&ms, h->recs[i].a, h->recs[i].b));
+      us[i] = 1e3 * ms;
+      names[i] = h->recs[i].name;
+    }
+    for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    h->recs.clear();
+    return rs;
+  } catch (const FdeFail& f) {
+    h->prof = false;
+    return fail(h, f);
+  } catch (...) {
+    h->prof = false;
+    return fail(h, FdeFail{FDE_ERR_CUDA, "unexpected exception"});
+  }
+}
 
 fde_status fde_profile_unit(fde_handle h, const double* x, double* y, double* z, int32_t reps, void* flush,
                             int64_t flush_bytes, int32_t max_kernels, int32_t* count, double* us,

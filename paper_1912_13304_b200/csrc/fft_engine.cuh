@@ -94,7 +94,9 @@ struct FftGeom {
   static constexpr int L = 1 << K, R = 1 << k, P = L >> k;
   static constexpr int NP = ceil_div_c(K, k);
   static constexpr int PAD_SHIFT = 4;  // one 16-byte pad slot per 16 points
-  static constexpr int SM_STRIDE = L + (L >> PAD_SHIFT) + 2;  // per-group smem stride (double2)
+  // per-group smem stride (double2): fits phys() and nat(); = 4 (mod 8) so that the
+  // interleaved column groups of a quarter-warp hit disjoint banks
+  static constexpr int SM_STRIDE = L + (L >> 3) + 4;
   __host__ __device__ static constexpr int lo(int i) { return K - (i + 1) * k > 0 ? K - (i + 1) * k : 0; }
   __host__ __device__ static constexpr int ka(int i) { return K - i * k - lo(i); }
   __device__ __forceinline__ static int pos(int t, int i, int q) {
@@ -102,6 +104,10 @@ struct FftGeom {
     return ((t >> l) << (l + k)) | (q << l) | (t & ((1 << l) - 1));
   }
   __device__ __forceinline__ static int phys(int p) { return p + (p >> PAD_SHIFT); }
+  // natural-order line staging (DST pre/post, outputs): one pad slot per 8
+  // points, so that per-thread chunks of 4 or 8 consecutive points (stride 4.5
+  // or 9 slots between lanes) and consecutive points are both conflict-free
+  __device__ __forceinline__ static int nat(int p) { return p + (p >> 3); }
 };
 
 __device__ __forceinline__ int bitrev_dev(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }

@@ -577,7 +577,7 @@ __global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const doub
 //   KM_GATE  no vector work; CTAs of finished RHS exit
 // Partials: kpart[(rhs*3 + slot)*KPMAX + blockIdx.x]; the last CTA of each RHS
 // (ticket) sums them in fixed order (deterministic) and updates SolveState.
-enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16 };
+enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16, KM_INIT = 32 };
 constexpr int KPMAX = 4096;   // CTAs per RHS of one line kernel
 
 struct KryFuse {
@@ -625,17 +625,52 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // all threads of the last CTA sum the partials (fixed order: thread-strided
+  // sums, then warps, then warp totals), loads of all slots in flight together
   __shared__ double tot[3];
-  for (int i = wid; i < 3; i += nw) {  // one warp per slot (blocks may have < 3 warps)
+  double sl[3] = {0.0, 0.0, 0.0};
+  const double* pr = k.part + (size_t)rhs * 3 * KPMAX;
+#pragma unroll 4
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    sl[0] += __ldcg(pr + b);
+    sl[1] += __ldcg(pr + KPMAX + b);
+    sl[2] += __ldcg(pr + 2 * KPMAX + b);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double v = warp_sum(sl[i]);
+    if (lane == 0) red[i * 32 + wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
     double s = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(k.part + ((size_t)rhs * 3 + i) * KPMAX + b);
-    s = warp_sum(s);
-    if (lane == 0) tot[i] = s;
+    for (int w = 0; w < nw; ++w) s += red[threadIdx.x * 32 + w];
+    tot[threadIdx.x] = s;
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
   k.ctr->tickets[rhs * 8 + 1] = 0u;
   SolveState& s = k.st[rhs];
+  if (k.mode & KM_INIT) {  // start of the sine-domain PCG: ‖b̂‖ and ρ = r̂·ẑ
+    s.bnorm = sqrt(tot[1]);
+    s.rho = tot[2];
+    s.betac = 0.0;
+    s.iters = 0;
+    s.converged = 0;
+    s.status = ST_OK;
+    s.restarts = 0;
+    s.rnorm = 1.0;
+    if (!(s.bnorm > 0.0)) {
+      s.converged = (s.bnorm == 0.0);
+      if (!(s.bnorm == 0.0)) s.status = ST_NONFINITE;
+      s.rnorm = 0.0;
+      finish_rhs(k.ctr, s);
+    } else if (!(s.rho > 0.0)) {
+      s.status = isfinite(s.rho) ? ST_NOT_SPD : ST_NONFINITE;
+      finish_rhs(k.ctr, s);
+    }
+    return;
+  }
   if (k.mode & KM_PQ) {
     const double pq = tot[0];
     if (!(pq > 0.0)) {

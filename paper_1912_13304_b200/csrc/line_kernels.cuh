@@ -43,6 +43,7 @@ struct LineArgs {
   const double* Fx;       // 2D τ (columns): cx·F_α(θ_i), i = 0..n-1
   const double* Fy;       // 2D τ (columns): cy·F_β(θ_j), j = 0..n-1
   double fscale;          // 2D τ: multiplier scale folded with 1/F
+  double oscale;          // DST kernels: output scale (0 = 1)
   int probe;              // phase-probe slot (FDE_PROBES builds only)
   KryFuse kf;             // fused PCG vector work (krylov_kernels.cuh); kf.mode = 0: none
 };
@@ -242,6 +243,10 @@ k_toeplitz_lines(LineArgs a) {
 
 __device__ __forceinline__ void store_pair(const LineArgs& a, const Line& A0, const Line& A1, bool v0, bool v1, int e,
                                            double r0, double r1) {
+  if (a.oscale != 0.0) {
+    r0 *= a.oscale;
+    r1 *= a.oscale;
+  }
   if (v0) {
     if (a.dpost) r0 *= __ldg(a.dpost + A0.fbase + e * A0.stride);
     a.y[A0.base + (long long)e * A0.stride] = r0;

@@ -1,0 +1,248 @@
+// Sine-domain PCG for constant coefficients (SURVEY §7 hard part (d)).
+//
+// With S = S_n symmetric and orthogonal (S² = I), the τ
+// preconditioner P = (S⊗S) diag(F) (S⊗S) is diagonal in the sine
+// basis, and the operator of P:L195-196 with constant d, e becomes
+//   Â = (S⊗S) A (S⊗S) = νI + I⊗(S T̃_α S) + (S T̃_β S)⊗I,
+// i.e. one 1D operator S T̃ S per line direction. PCG on x̂ = (S⊗S)x, b̂ =
+// (S⊗S)b produces the same iterates as PCG on A x = b with P (exact
+// arithmetic; orthogonality keeps every dot product and norm), so iteration
+// counts and the stopping test are unchanged. Each line of each direction is
+// transformed ONCE per iteration: DST -> Toeplitz (circulant embedding) ->
+// DST in shared memory, instead of the separate matvec and τ passes.
+// Vectors are kept in the unnormalised DST scale (D = sqrt(2m) S, D⊗D =
+// 2m S⊗S): the 1/(2m) of D T D / (2m) = S T S is folded into the multiplier
+// μ_s, and norms only change by the common factor 2m (ratios unchanged).
+#pragma once
+#include "dst_kernels.cuh"
+
+namespace fde {
+
+// symbol F at element e of line l (2D rows: x index e, y index l; 2D cols:
+// x index l, y index e; 1D: Fy == nullptr)
+template <bool COL>
+__device__ __forceinline__ double symbol_at(const LineArgs& a, int l, int e) {
+  if (!a.Fy) return a.Fx[e];
+  return COL ? a.Fx[l] + a.Fy[e] : a.Fx[e] + a.Fy[l];
+}
+
+// MODE 0: 2D row pass:   p̂ = r̂/F + β p̂ (written back), y = (S T̃_α S) p̂ along rows
+// MODE 1: 2D column pass: y = q̂ = ν p̂ + yin + (S T̃_β S) p̂ along columns, partial p̂·q̂
+// MODE 2: 1D:            p̂ = r̂/F + β p̂, y = q̂ = ν p̂ + (S T̃ S) p̂, partial p̂·q̂
+// a.x = r̂ (MODE 0/2) or p̂ (MODE 1); a.kf.p = p̂; a.mu = the sine-domain μ_s.
+template <int KM, bool COL, int FPC, int MODE>
+__global__ void __launch_bounds__(FPC * (1 << (KM - 3)), min_blocks_for(FPC * (1 << (KM - 3))))
+k_sineop_lines(LineArgs a) {
+  using GD = FftGeom<KM, 3>;      // DST: length-m FFT, 8 points per thread
+  using GT = FftGeom<KM + 1, 4>;  // Toeplitz: length-2m FFT, 16 points per thread
+  static_assert(GD::P == GT::P, "one thread layout for both transforms");
+  using M = LineMap<GD, COL, FPC>;
+  constexpr int m = GD::L, P = GD::P, RD = GD::R;
+  extern __shared__ double2 smem_all[];
+  if (kry_skip(a)) return;
+  const int f = M::group(), t = M::lane();
+  double2* sm = smem_all + (size_t)f * GT::SM_STRIDE;
+  double2* smW = smem_all + (size_t)FPC * GT::SM_STRIDE + (size_t)f * GD::SM_STRIDE;
+  double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * (GT::SM_STRIDE + (MODE == 1 ? GD::SM_STRIDE : 0)));
+  const TwSrc twd{nullptr, a.twpm}, twt{nullptr, a.twp};
+  const int g = blockIdx.x * FPC + f;
+  const int l0 = 2 * g, l1 = 2 * g + 1;
+  const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
+  const int n = m - 1;
+  const Line A0 = line_of<COL>(v0 ? l0 : 0, blockIdx.y, n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, blockIdx.y, n, a.N);
+
+  // 1. stage p̂ in shared memory (natural order, position e+1)
+  const double beta = MODE != 1 ? a.kf.st[blockIdx.y].betac : 0.0;
+#pragma unroll
+  for (int i = 0; i < RD; ++i) {
+    const int e = t + P * i;
+    if (e < n) {
+      const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
+      double p0 = 0.0, p1 = 0.0;
+      if (MODE != 1) {  // p̂ = ẑ + β p̂ with ẑ = r̂ / F (the τ-solve is diagonal here)
+        if (v0) { p0 = fma(beta, a.kf.p[o0], __ldg(a.x + o0) * fast_rcp(symbol_at<COL>(a, l0, e))); a.kf.p[o0] = p0; }
+        if (v1) { p1 = fma(beta, a.kf.p[o1], __ldg(a.x + o1) * fast_rcp(symbol_at<COL>(a, l1, e))); a.kf.p[o1] = p1; }
+      } else {
+        if (v0) p0 = __ldg(a.x + o0);
+        if (v1) p1 = __ldg(a.x + o1);
+      }
+      sm[GD::nat(e + 1)] = make_double2(p0, p1);
+    }
+  }
+  if (MODE == 1 && a.yin) {  // the row pass's result streams in for the epilogue (chunk layout)
+#pragma unroll
+    for (int i = 0; i < RD; ++i) {
+      const int e = RD * t + i - 1;
+      if (e >= 0 && e < n) {
+        if (v0) cp_async8(&smW[GD::nat(e)].x, a.yin + A0.base + (long long)e * A0.stride);
+        if (v1) cp_async8(&smW[GD::nat(e)].y, a.yin + A1.base + (long long)e * A1.stride);
+      }
+    }
+  }
+  if (t == 0) sm[GD::nat(0)] = make_double2(0.0, 0.0);
+  __syncthreads();
+
+  // 2. DST #1 (D p̂)
+  double2 vd[RD];
+  dstm_pre_smem<GD, KM, 3>(vd, sm, t, a.sinm);
+  dif_chain<GD, -1, false>(vd, sm, t, twd);
+  double g0[RD], g1[RD];
+  dstm_post<GD, COL, FPC>(vd, sm, scr, t, f, g0, g1);
+
+  // 3. to the Toeplitz input layout (element e at position e, zero padded to 2m)
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < RD; ++i) {
+    const int idx = RD * t + i;
+    if (idx >= 1) sm[GT::nat(idx - 1)] = make_double2(g0[i], g1[i]);
+  }
+  __syncthreads();
+  double2 v[GT::R];
+#pragma unroll
+  for (int q = 0; q < GT::R / 2; ++q) {
+    const int p = q * P + t;
+    v[q] = p < n ? sm[GT::nat(p)] : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int q = GT::R / 2; q < GT::R; ++q) v[q] = make_double2(0.0, 0.0);
+  __syncthreads();
+
+  // 4. T̃ via the circulant embedding (μ_s carries d or e, 1/L and 1/(2m))
+  dif_chain<GT, -1, true>(v, sm, t, twt);
+#pragma unroll
+  for (int q = 0; q < GT::R; ++q) v[q] = c_mul(v[q], a.mu[(t << 4) | q]);
+  dit_chain<GT, +1>(v, sm, t, twt);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < GT::R / 2; ++q) {
+    const int p = q * P + t;
+    if (p < n) sm[GD::nat(p + 1)] = v[q];
+  }
+  if (t == 0) sm[GD::nat(0)] = make_double2(0.0, 0.0);
+  __syncthreads();
+
+  // 5. DST #2
+  dstm_pre_smem<GD, KM, 3>(vd, sm, t, a.sinm);
+  dif_chain<GD, -1, false>(vd, sm, t, twd);
+  dstm_post<GD, COL, FPC>(vd, sm, scr, t, f, g0, g1);
+
+  // 6. epilogue
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (MODE == 1) {
+    // columns: this lane owns rows e = RD t + i - 1 of its two columns
+    if (a.yin) cp_async_wait_all();
+#pragma unroll
+    for (int i = 0; i < RD; ++i) {
+      const int e = RD * t + i - 1;
+      if (e < 0) continue;
+      if (v0) {
+        const long long o = A0.base + (long long)e * A0.stride;
+        const double pv = a.kf.p[o];
+        const double qv = fma(a.nu, pv, g0[i] + (a.yin ? smW[GD::nat(e)].x : 0.0));
+        a.y[o] = qv;
+        acc[0] = fma(pv, qv, acc[0]);
+      }
+      if (v1) {
+        const long long o = A1.base + (long long)e * A1.stride;
+        const double pv = a.kf.p[o];
+        const double qv = fma(a.nu, pv, g1[i] + (a.yin ? smW[GD::nat(e)].y : 0.0));
+        a.y[o] = qv;
+        acc[0] = fma(pv, qv, acc[0]);
+      }
+    }
+  } else {
+    // rows: stage through shared memory for coalesced stores
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RD; ++i) sm[GD::nat(RD * t + i)] = make_double2(g0[i], g1[i]);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RD; ++i) {
+      const int e = t + P * i;
+      if (e >= n) continue;
+      const double2 o = sm[GD::nat(e + 1)];
+      const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
+      if (MODE == 0) {
+        if (v0) a.y[o0] = o.x;
+        if (v1) a.y[o1] = o.y;
+      } else {  // 1D: q̂ = ν p̂ + (S T̃ S) p̂, p̂·q̂
+        if (v0) {
+          const double pv = a.kf.p[o0], qv = fma(a.nu, pv, o.x);
+          a.y[o0] = qv;
+          acc[0] = fma(pv, qv, acc[0]);
+        }
+        if (v1) {
+          const double pv = a.kf.p[o1], qv = fma(a.nu, pv, o.y);
+          a.y[o1] = qv;
+          acc[0] = fma(pv, qv, acc[0]);
+        }
+      }
+    }
+  }
+  if (MODE != 0) kry_reduce_finalize(a.kf, acc);
+}
+
+// F at (i, j) in the sine domain (1D: Fy == nullptr)
+// Element loops below run rows j over blocks (2D) so no integer division is
+// needed; 1D is one row.
+#define FDE_SINE_LOOP(BODY)                                                       \
+  if (dims == 2) {                                                                \
+    for (int j = blockIdx.x; j < n; j += gridDim.x) {                             \
+      const double fy = Fy[j];                                                    \
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {                         \
+        const size_t e = (size_t)j * n + i;                                       \
+        const double F = Fx[i] + fy;                                              \
+        BODY                                                                      \
+      }                                                                           \
+    }                                                                             \
+  } else {                                                                        \
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) { \
+      const size_t e = (size_t)i;                                                 \
+      const double F = Fx[i];                                                     \
+      BODY                                                                        \
+    }                                                                             \
+  }
+
+// PCG vector step in the sine domain: x̂ += α p̂, r̂ -= α q̂, partials ‖r̂‖² and
+// r̂·ẑ = Σ r̂²/F (the diagonal preconditioner), finalised like KM_XR | KM_RZ.
+__global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, const double* __restrict__ Fx,
+                                                 const double* __restrict__ Fy) {
+  const int rhs = blockIdx.y;
+  if (!k.st[rhs].cyc_active) return;
+  const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * n : (size_t)n);
+  const double al = k.st[rhs].alpha;
+  double* __restrict__ xr = k.x + o;
+  double* __restrict__ rr = k.r + o;
+  const double* __restrict__ pr = k.p + o;
+  const double* __restrict__ qr = k.q + o;
+  double acc[3] = {0.0, 0.0, 0.0};
+  FDE_SINE_LOOP({
+    const double rv = fma(-al, qr[e], rr[e]);
+    rr[e] = rv;
+    xr[e] = fma(al, pr[e], xr[e]);
+    acc[1] = fma(rv, rv, acc[1]);
+    acc[2] = fma(rv * rv, fast_rcp(F), acc[2]);
+  })
+  kry_reduce_finalize(k, acc);
+}
+
+// sine-domain PCG start: x̂ = 0, p̂ = 0, ‖b̂‖, ρ = Σ r̂²/F, β = 0 (r̂ = b̂ already formed)
+__global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, const double* __restrict__ Fx,
+                                                   const double* __restrict__ Fy) {
+  const int rhs = blockIdx.y;
+  const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * n : (size_t)n);
+  double acc[3] = {0.0, 0.0, 0.0};
+  FDE_SINE_LOOP({
+    const double rv = k.r[o + e];
+    k.x[o + e] = 0.0;
+    k.p[o + e] = 0.0;
+    acc[1] = fma(rv, rv, acc[1]);
+    acc[2] = fma(rv * rv, fast_rcp(F), acc[2]);
+  })
+  // reuse the fused finalisation: slot 1 -> ‖b̂‖, slot 2 -> ρ (mode bits select the init path)
+  KryFuse ki = k;
+  ki.mode = KM_INIT;
+  kry_reduce_finalize(ki, acc);
+}
+
+}  // namespace fde

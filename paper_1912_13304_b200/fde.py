@@ -81,6 +81,10 @@ lib.fde_profile_unit.argtypes = [_H, _P, _P, _P, ctypes.c_int32, _P, ctypes.c_in
                                  ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double),
                                  ctypes.POINTER(ctypes.c_char_p)]
 lib.fde_profile_unit.restype = ctypes.c_int
+lib.fde_profile_solve.argtypes = [_H, _P, _P, ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                  ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(fde_stats)]
+lib.fde_profile_solve.restype = ctypes.c_int
 
 
 def fde_status_str(s: int) -> str:
@@ -190,6 +194,19 @@ class Fde:
         self._check(lib.fde_profile_unit(self._h, _ptr(x), _ptr(y), _ptr(z), reps, fp or None, fb, MAXK,
                                          ctypes.byref(cnt), us, names))
         return [(names[i].decode(), us[i]) for i in range(min(cnt.value, MAXK))]
+
+    def profile_solve(self, b, x, solver: str = "pcg", rtol: float = 1e-10, maxit: int = 5000, restart: int = 30):
+        """fde_profile_solve: one solve whose loop body carries CUDA events;
+        returns ([(name, µs of the last loop body)], stats)."""
+        MAXK = 256
+        us = (ctypes.c_double * MAXK)()
+        names = (ctypes.c_char_p * MAXK)()
+        cnt = ctypes.c_int32(0)
+        stats = (fde_stats * self.batch)()
+        self._check(lib.fde_profile_solve(self._h, _ptr(b), _ptr(x), rtol, maxit, 0 if solver == "pcg" else 1,
+                                          restart, MAXK, ctypes.byref(cnt), us, names, stats))
+        return ([(names[i].decode(), us[i]) for i in range(min(cnt.value, MAXK))],
+                [dict(iters=s.iters, converged=bool(s.converged)) for s in stats])
 
     def close(self):
         if self._h:
