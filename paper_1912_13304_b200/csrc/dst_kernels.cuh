@@ -62,14 +62,14 @@ __device__ __forceinline__ void dstm_post(double2 (&v)[G::R], double2* sm, doubl
   constexpr int m = G::L, P = G::P, k = G::k, C = G::R / 2;
   __syncthreads();  // the chain's last exchange reads are done
 #pragma unroll
-  for (int q = 0; q < G::R; ++q) sm[G::nat(bitrev_dev((t << k) | q, G::K))] = v[q];
+  for (int q = 0; q < G::R; ++q) sm[G::swz(bitrev_dev((t << k) | q, G::K))] = v[q];
   __syncthreads();
   double re0[C], re1[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const int kk = C * t + c;
-    const double2 Zk = sm[G::nat(kk)];
-    const double2 Zm = sm[G::nat((m - kk) & (m - 1))];
+    const double2 Zk = sm[G::swz(kk)];
+    const double2 Zm = sm[G::swz((m - kk) & (m - 1))];
     // V1 = Z_k + conj Z_{m-k} (= 2W¹_k), V2 = -i(Z_k - conj Z_{m-k}) (= 2W²_k)
     g0[2 * c] = Zm.y - Zk.y;    // G_{2kk} = -Im V1
     g1[2 * c] = Zk.x - Zm.x;    // G_{2kk} = -Im V2
@@ -104,16 +104,18 @@ __device__ __forceinline__ double2 dstm_pre(double sj, double a0, double b0, dou
 }
 
 // w of the packed pair for the DIF input positions j = (q << (KM-k)) | t from
-// the natural-order line pair in shared memory (sm[phys(0)] = 0); ends with a
-// barrier because the chain's first exchange overwrites sm.
+// the natural-order line pair in shared memory (element e = j-1 at swz(e); the
+// boundary values y_0 = y_m = 0); ends with a barrier because the chain's
+// first exchange overwrites sm.
 template <class G, int KM, int k>
 __device__ __forceinline__ void dstm_pre_smem(double2 (&v)[G::R], const double2* sm, int t, const double* sinm) {
   constexpr int m = G::L;
 #pragma unroll
   for (int q = 0; q < G::R; ++q) {
     const int j = (q << (KM - k)) | t;
-    const double2 yj = sm[G::nat(j)];
-    const double2 ym = sm[G::nat((m - j) & (m - 1))];   // j = 0: both are entry 0 = 0
+    const double2 z = make_double2(0.0, 0.0);
+    const double2 yj = j >= 1 ? sm[G::swz(j - 1)] : z;
+    const double2 ym = j >= 1 ? sm[G::swz(m - j - 1)] : z;
     v[q] = dstm_pre(__ldg(sinm + j), yj.x, ym.x, yj.y, ym.y);
   }
   __syncthreads();
@@ -177,10 +179,9 @@ k_dstm_lines(LineArgs a) {
         if (v0) y0 *= __ldg(a.dpre + A0.fbase + e * A0.stride);
         if (v1) y1 *= __ldg(a.dpre + A1.fbase + e * A1.stride);
       }
-      sm[G::nat(e + 1)] = make_double2(y0, y1);
+      sm[G::swz(e)] = make_double2(y0, y1);
     }
   }
-  if (t == 0) sm[G::nat(0)] = make_double2(0.0, 0.0);
   __syncthreads();
   dstm_pre_smem<G, KM, k>(v, sm, t, a.sinm);
   __syncwarp();
@@ -208,9 +209,8 @@ k_dstm_lines(LineArgs a) {
         s0 = a.fscale * fast_rcp(fx0 + fy);
         s1 = a.fscale * fast_rcp(fx1 + fy);
       }
-      sm[G::nat(idx)] = make_double2(s0 * g0[i], s1 * g1[i]);
+      sm[G::swz(idx - 1)] = make_double2(s0 * g0[i], s1 * g1[i]);
     }
-    if (t == 0) sm[G::nat(0)] = make_double2(0.0, 0.0);
     __syncthreads();
     dstm_pre_smem<G, KM, k>(v, sm, t, a.sinm);
     dif_chain<G, -1, false>(v, sm, t, tws);
@@ -229,13 +229,14 @@ k_dstm_lines(LineArgs a) {
     // rows: stage through shared memory for coalesced stores
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < R; ++i) sm[G::nat(2 * C * t + i)] = make_double2(g0[i], g1[i]);
+    for (int i = 0; i < R; ++i)
+      if (2 * C * t + i >= 1) sm[G::swz(2 * C * t + i - 1)] = make_double2(g0[i], g1[i]);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int e = t + P * i;
       if (e < m - 1) {
-        const double2 o = sm[G::nat(e + 1)];
+        const double2 o = sm[G::swz(e)];
         store_pair(a, A0, A1, v0, v1, e, o.x, o.y);
         if (rz) {  // r·z partial of the stored z (KM_RZ)
           const double z0 = a.dpost ? o.x * __ldg(a.dpost + A0.fbase + e * A0.stride) : o.x;

@@ -94,20 +94,28 @@ struct FftGeom {
   static constexpr int L = 1 << K, R = 1 << k, P = L >> k;
   static constexpr int NP = ceil_div_c(K, k);
   static constexpr int PAD_SHIFT = 4;  // one 16-byte pad slot per 16 points
-  // per-group smem stride (double2): fits phys() and nat(); = 4 (mod 8) so that the
-  // interleaved column groups of a quarter-warp hit disjoint banks
-  static constexpr int SM_STRIDE = L + (L >> 3) + 4;
+  // per-group smem stride (double2): phys() and swz() permute within [0, L);
+  // = 4 (mod 8) so that the interleaved column groups of a quarter-warp hit
+  // disjoint bank halves
+  static constexpr int SM_STRIDE = L + 4;
   __host__ __device__ static constexpr int lo(int i) { return K - (i + 1) * k > 0 ? K - (i + 1) * k : 0; }
   __host__ __device__ static constexpr int ka(int i) { return K - i * k - lo(i); }
   __device__ __forceinline__ static int pos(int t, int i, int q) {
     const int l = lo(i);
     return ((t >> l) << (l + k)) | (q << l) | (t & ((1 << l) - 1));
   }
-  __device__ __forceinline__ static int phys(int p) { return p + (p >> PAD_SHIFT); }
-  // natural-order line staging (DST pre/post, outputs): one pad slot per 8
-  // points, so that per-thread chunks of 4 or 8 consecutive points (stride 4.5
-  // or 9 slots between lanes) and consecutive points are both conflict-free
-  __device__ __forceinline__ static int nat(int p) { return p + (p >> 3); }
+  // exchange layout: XOR swizzle p ^ ((p >> k) & 7). For every pass pattern
+  // pos(t, i, q) the 8 lanes of a quarter-warp (one 128-bit shared-memory
+  // transaction) fall on 8 distinct 16-byte bank groups: lo >= 3 passes touch
+  // aligned runs of 8, lo = 0..2 passes carry the varying lane bits at
+  // [k, k+3) which the swizzle folds into the low bits.
+  __device__ __forceinline__ static int phys(int p) { return p ^ ((p >> k) & 7); }
+  // natural-order line staging (DST pre/post, outputs), indexed by element:
+  // an XOR swizzle inside aligned 64-slot blocks (no padding). Aligned runs of
+  // 8 consecutive elements stay in one 128-byte line (a quarter-warp of 16-byte
+  // accesses is conflict-free) and per-lane chunks of 4 or 8 consecutive
+  // elements land on distinct bank groups.
+  __device__ __forceinline__ static int swz(int p) { return p ^ ((p >> 3) & 7); }
 };
 
 __device__ __forceinline__ int bitrev_dev(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }

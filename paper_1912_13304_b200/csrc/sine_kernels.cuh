@@ -66,7 +66,7 @@ k_sineop_lines(LineArgs a) {
         if (v0) p0 = __ldg(a.x + o0);
         if (v1) p1 = __ldg(a.x + o1);
       }
-      sm[GD::nat(e + 1)] = make_double2(p0, p1);
+      sm[GD::swz(e)] = make_double2(p0, p1);
     }
   }
   if (MODE == 1 && a.yin) {  // the row pass's result streams in for the epilogue (chunk layout)
@@ -74,12 +74,11 @@ k_sineop_lines(LineArgs a) {
     for (int i = 0; i < RD; ++i) {
       const int e = RD * t + i - 1;
       if (e >= 0 && e < n) {
-        if (v0) cp_async8(&smW[GD::nat(e)].x, a.yin + A0.base + (long long)e * A0.stride);
-        if (v1) cp_async8(&smW[GD::nat(e)].y, a.yin + A1.base + (long long)e * A1.stride);
+        if (v0) cp_async8(&smW[GD::swz(e)].x, a.yin + A0.base + (long long)e * A0.stride);
+        if (v1) cp_async8(&smW[GD::swz(e)].y, a.yin + A1.base + (long long)e * A1.stride);
       }
     }
   }
-  if (t == 0) sm[GD::nat(0)] = make_double2(0.0, 0.0);
   __syncthreads();
 
   // 2. DST #1 (D p̂)
@@ -94,14 +93,14 @@ k_sineop_lines(LineArgs a) {
 #pragma unroll
   for (int i = 0; i < RD; ++i) {
     const int idx = RD * t + i;
-    if (idx >= 1) sm[GT::nat(idx - 1)] = make_double2(g0[i], g1[i]);
+    if (idx >= 1) sm[GT::swz(idx - 1)] = make_double2(g0[i], g1[i]);
   }
   __syncthreads();
   double2 v[GT::R];
 #pragma unroll
   for (int q = 0; q < GT::R / 2; ++q) {
     const int p = q * P + t;
-    v[q] = p < n ? sm[GT::nat(p)] : make_double2(0.0, 0.0);
+    v[q] = p < n ? sm[GT::swz(p)] : make_double2(0.0, 0.0);
   }
 #pragma unroll
   for (int q = GT::R / 2; q < GT::R; ++q) v[q] = make_double2(0.0, 0.0);
@@ -116,9 +115,8 @@ k_sineop_lines(LineArgs a) {
 #pragma unroll
   for (int q = 0; q < GT::R / 2; ++q) {
     const int p = q * P + t;
-    if (p < n) sm[GD::nat(p + 1)] = v[q];
+    if (p < n) sm[GD::swz(p)] = v[q];
   }
-  if (t == 0) sm[GD::nat(0)] = make_double2(0.0, 0.0);
   __syncthreads();
 
   // 5. DST #2
@@ -138,14 +136,14 @@ k_sineop_lines(LineArgs a) {
       if (v0) {
         const long long o = A0.base + (long long)e * A0.stride;
         const double pv = a.kf.p[o];
-        const double qv = fma(a.nu, pv, g0[i] + (a.yin ? smW[GD::nat(e)].x : 0.0));
+        const double qv = fma(a.nu, pv, g0[i] + (a.yin ? smW[GD::swz(e)].x : 0.0));
         a.y[o] = qv;
         acc[0] = fma(pv, qv, acc[0]);
       }
       if (v1) {
         const long long o = A1.base + (long long)e * A1.stride;
         const double pv = a.kf.p[o];
-        const double qv = fma(a.nu, pv, g1[i] + (a.yin ? smW[GD::nat(e)].y : 0.0));
+        const double qv = fma(a.nu, pv, g1[i] + (a.yin ? smW[GD::swz(e)].y : 0.0));
         a.y[o] = qv;
         acc[0] = fma(pv, qv, acc[0]);
       }
@@ -154,13 +152,14 @@ k_sineop_lines(LineArgs a) {
     // rows: stage through shared memory for coalesced stores
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < RD; ++i) sm[GD::nat(RD * t + i)] = make_double2(g0[i], g1[i]);
+    for (int i = 0; i < RD; ++i)
+      if (RD * t + i >= 1) sm[GD::swz(RD * t + i - 1)] = make_double2(g0[i], g1[i]);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
       const int e = t + P * i;
       if (e >= n) continue;
-      const double2 o = sm[GD::nat(e + 1)];
+      const double2 o = sm[GD::swz(e)];
       const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
       if (MODE == 0) {
         if (v0) a.y[o0] = o.x;
