@@ -164,7 +164,7 @@ bool is_device_ptr(const void* p) {
 template <int K, bool COL, int NBUF>
 struct LaunchCfg {
   using G = FftGeom<K, KR>;
-  static constexpr int SPG = G::SM_STRIDE * 16 * NBUF + (COL ? (G::L / 2) * 16 : 0);  // smem bytes per FFT group (+ yin staging)
+  static constexpr int SPG = G::SM_STRIDE * 16 + (COL ? (G::L / 2) * 16 : 0);  // smem bytes per FFT group (+ yin staging)
   static constexpr int SMEM_CAP = 200 * 1024;
   static constexpr int BY_SMEM = (SMEM_CAP - TW_SMEM_QUARTER * (G::L / 4) * 16) / SPG > 0 ? (SMEM_CAP - TW_SMEM_QUARTER * (G::L / 4) * 16) / SPG : 1;
   static constexpr int BY_THR = 512 / G::P > 0 ? 512 / G::P : 1;  // <= 512 threads: 128 registers/thread
@@ -244,6 +244,7 @@ struct fde_handle_s {
   double* part = nullptr;
   double *kx = nullptr, *kb = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kq = nullptr;
   double* kpart = nullptr;  // fused-kernel partials [batch][3][KPMAX]
+  double2* zscr = nullptr;  // variable Toeplitz spectrum scratch [batch][pairs][L]
   double* V = nullptr;
   int V_cols = 0;
   // graphs
@@ -293,6 +294,7 @@ LineArgs base_args(fde_handle h) {
   a.twp = h->twp;
   a.twpm = h->twpm;
   a.sinm = h->sinm;
+  a.zscr = h->zscr;
 #ifdef FDE_PROBES
   a.probe = g_probe_next++ & 7;
 #endif
@@ -699,6 +701,7 @@ void build(fde_handle h, const fde_desc* d) {
   }
 
   const size_t ve = h->vec_elems();
+  if (h->var_x || h->var_y) h->zscr = h->dalloc<double2>((size_t)h->batch * (m / 2 + 64) * L);
   h->wx = h->dalloc<double>(ve);
   h->t1 = h->dalloc<double>(ve);
   h->t2 = h->dalloc<double>(ve);
@@ -1086,8 +1089,7 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
   const int* gU = &h->ctr->unfinished;
   const size_t vs = h->vec_elems();
   double* V = h->V;
-  k_gm_scale<<<VGRID, RED_THREADS, 0, h->st>>>(va, V);
-  h->launches++;
+  launch_named(h, "gm_scale", [&] { k_gm_scale<<<VGRID, RED_THREADS, 0, h->st>>>(va, V); });
   for (int j = 0; j < restart; ++j) {
     double* Vj = V + (size_t)j * vs;
     double* Vn = V + (size_t)(j + 1) * vs;
@@ -1098,18 +1100,16 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
       op_matvec(h, Vj, h->kq, gA);
       op_tau(h, h->kq, Vn, gA);
     }
-    k_gm_mdot<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j);
-    k_gm_upd_mdot<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j);
-    k_gm_upd_norm<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j);
-    h->launches += 3;
-    if (j + 1 < restart) {
-      k_gm_scale<<<VGRID, RED_THREADS, 0, h->st>>>(va, Vn);
-      h->launches++;
-    }
+    launch_named(h, "gm_mdot", [&] { k_gm_mdot<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j); });
+    if (j < 32)
+      launch_named(h, "gm_upd_mdot", [&] { k_gm_upd_mdot32<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j); });
+    else
+      launch_named(h, "gm_upd_mdot", [&] { k_gm_upd_mdot<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j); });
+    launch_named(h, "gm_upd_norm", [&] { k_gm_upd_norm<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j); });
+    if (j + 1 < restart) launch_named(h, "gm_scale", [&] { k_gm_scale<<<VGRID, RED_THREADS, 0, h->st>>>(va, Vn); });
   }
   // end of cycle: x += P⁻¹(V y) (right) or V y (left); restart residual
-  k_gm_lincomb<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, h->kp);
-  h->launches++;
+  launch_named(h, "gm_lincomb", [&] { k_gm_lincomb<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, h->kp); });
   if (!left) {
     op_tau(h, h->kp, h->kz, gU);
     k_gm_xupd<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kz, h->kx);

@@ -414,6 +414,50 @@ __global__ void k_gm_upd_mdot(VecArgs a, const double* __restrict__ V, size_t vs
   if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, a.gs[rb].h2);
 }
 
+// CGS pass 1 update + pass 2 dots in ONE pass over V (j < 32): per element,
+// w' = w - Σ h_i V_i, then h2_i += V_i w' with the V_i values still in
+// registers (the vectors are read from HBM once instead of twice)
+__global__ void __launch_bounds__(RED_THREADS) k_gm_upd_mdot32(VecArgs a, const double* __restrict__ V, size_t vstride,
+                                                               double* __restrict__ w, int j) {
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  const int nv = j + 1;
+  __shared__ double hs[32];
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) hs[i] = i < nv ? __ldcg(&a.gs[rb].h[i]) : 0.0;
+  __syncthreads();
+  double acc[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (long long)gridDim.x * blockDim.x) {
+    double vv[32];
+    double wv = w[o + e];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      vv[i] = i < nv ? __ldg(V + (size_t)i * vstride + o + e) : 0.0;
+      wv = fma(-hs[i], vv[i], wv);
+    }
+    w[o + e] = wv;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = fma(vv[i], wv, acc[i]);
+  }
+  // block sums of the nv dots in chunks of 8 (fixed order), partials, last block
+  __shared__ double red[MD_CH * 32];
+  double* part = a.part + (size_t)rb * (MAX_RESTART + 1) * RED_BLOCKS;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (8 * c >= nv) break;
+    double ch[MD_CH];
+#pragma unroll
+    for (int i = 0; i < MD_CH; ++i) ch[i] = acc[8 * c + i];
+    block_sum<MD_CH>(ch, red);
+    if (threadIdx.x == 0)
+      for (int i = 0; i < MD_CH && 8 * c + i < nv; ++i) part[(size_t)(8 * c + i) * RED_BLOCKS + blockIdx.x] = ch[i];
+  }
+  if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, a.gs[rb].h2);
+}
+
 // CGS pass 2 update + norm + Arnoldi/Givens step (thread 0 of the last block)
 __global__ void k_gm_upd_norm(VecArgs a, const double* __restrict__ V, size_t vstride, double* w, int j) {
   if (a.ctr->active == 0) return;

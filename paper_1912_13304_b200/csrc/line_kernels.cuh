@@ -44,6 +44,7 @@ struct LineArgs {
   const double* Fy;       // 2D τ (columns): cy·F_β(θ_j), j = 0..n-1
   double fscale;          // 2D τ: multiplier scale folded with 1/F
   double oscale;          // DST kernels: output scale (0 = 1)
+  double2* zscr;          // variable Toeplitz: global scratch for the forward spectrum (L per line pair)
   int probe;              // phase-probe slot (FDE_PROBES builds only)
   KryFuse kf;             // fused PCG vector work (krylov_kernels.cuh); kf.mode = 0: none
 };
@@ -121,11 +122,10 @@ k_toeplitz_lines(LineArgs a) {
   double2* smem = smem_all + TW_SMEM_QUARTER * (G::L >> 2);
   const TwSrc tws{sm_tw, a.twp};
   const int f = M::group(), t = M::lane();
-  double2* sm = smem + (size_t)f * G::SM_STRIDE * (VAR ? 2 : 1);
-  double2* smZ = sm + G::SM_STRIDE;
+  double2* sm = smem + (size_t)f * G::SM_STRIDE;
   // column pass: the other direction's partial (yin) streams into shared memory
   // while the transform runs (one slot per epilogue position of this thread)
-  double2* smY = smem + (size_t)FPC * G::SM_STRIDE * (VAR ? 2 : 1) + (size_t)f * (G::L / 2);
+  double2* smY = smem + (size_t)FPC * G::SM_STRIDE + (size_t)f * (G::L / 2);
   FDE_PROBE(0);
   const int g = blockIdx.x * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
@@ -179,10 +179,15 @@ k_toeplitz_lines(LineArgs a) {
     for (int q = 0; q < G::R; ++q) v[q] = c_mul(v[q], a.mu[(t << k) | q]);
     dit_chain<G, +1>(v, sm, t, tws);
   } else {
+    // the forward spectrum is parked in a global (L2-resident) scratch for the
+    // second inverse transform, so one shared-memory buffer per pair suffices
+    // and every pair of a pass stays resident; lane-major layout (coalesced),
+    // own positions only (no barrier needed for the reload)
+    double2* zs = a.zscr + ((size_t)(blockIdx.y * gridDim.x) * FPC + g) * G::L;
 #pragma unroll
     for (int q = 0; q < G::R; ++q) {
       const int s = (t << k) | q;
-      smZ[s] = v[q];  // own positions: no barrier needed for the later reload
+      zs[q * G::P + t] = v[q];
       v[q] = c_scale(v[q], a.lamS[s]);
     }
     dit_chain<G, +1>(v, sm, t, tws);
@@ -192,7 +197,7 @@ k_toeplitz_lines(LineArgs a) {
 #pragma unroll
     for (int q = 0; q < G::R; ++q) {
       const int s = (t << k) | q;
-      const double2 z = smZ[s];
+      const double2 z = zs[q * G::P + t];
       const double lk = a.lamK[s];
       v[q] = make_double2(-lk * z.y, lk * z.x);  // i·Im λ ⊙ Z
     }
