@@ -230,13 +230,13 @@ k_toeplitz_lines(LineArgs a) {
     // nu = 0 then), explicit otherwise; the partial of the other direction is read here with
     // plain loads (not hoisted above the transform by the compiler)
     if (v0) {
-      if (a.nu != 0.0) r0 = fma(a.nu, a.x[o0], r0);
+      if (a.nu != 0.0) r0 = fma(a.nu, pupd ? a.kf.p[o0] : a.x[o0], r0);  // ν p, not ν z, under KM_PUPD
       if (a.yin) r0 += COL ? smY[p].x : a.yin[o0];
       a.y[o0] = r0;
       if (pq) acc[0] = fma(a.kf.p[o0], r0, acc[0]);
     }
     if (v1) {
-      if (a.nu != 0.0) r1 = fma(a.nu, a.x[o1], r1);
+      if (a.nu != 0.0) r1 = fma(a.nu, pupd ? a.kf.p[o1] : a.x[o1], r1);
       if (a.yin) r1 += COL ? smY[p].y : a.yin[o1];
       a.y[o1] = r1;
       if (pq) acc[0] = fma(a.kf.p[o1], r1, acc[0]);

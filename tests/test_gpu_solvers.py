@@ -119,3 +119,113 @@ def test_paper_table1_iterations_on_gpu(torch_cuda):
             u = x[0]
         h.close()
         assert abs(its / ex["M"] - printed) <= 0.15, (alpha, its / ex["M"])
+
+
+def _solve_with_env(torch, p, env):
+    """A solve on a handle created under an environment override
+    (FDE_PCG=standard selects the standard-domain fused PCG)."""
+    import os
+    from paper_1912_13304_b200 import fde
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        h = fde.Fde.from_problem(p)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    b = torch.from_numpy(p.rhs.copy()).cuda()
+    x = torch.zeros_like(b)
+    st, stats = h.pcg(b, x, p.rtol, p.maxit)
+    torch.cuda.synchronize()
+    out = x.cpu().numpy()
+    h.close()
+    return stats, out
+
+
+@pytest.mark.parametrize("cfg,n,batch", [(1, 127, 2), (3, 63, 1), (5, 255, 3), (3, 511, 1)])
+def test_pcg_sine_domain_and_standard_paths_agree_with_oracle(torch_cuda, cfg, n, batch):
+    """Constant coefficients + τ: fde_pcg runs PCG in the sine basis (DESIGN.md
+    §5.4); FDE_PCG=standard forces the standard-domain fused iteration. Both
+    must match the oracle's PCG (iterations ±1, solution 1e-9)."""
+    p = W.config(cfg, n=n, batch=batch)
+    s = oracle_system(p)
+    ref = oracle_solve(p, s, "pcg")
+    for env in ({}, {"FDE_PCG": "standard"}):
+        stats, x = _solve_with_env(torch_cuda, p, env)
+        for b in range(batch):
+            xo, it_o, conv_o, _ = ref[b]
+            assert stats[b]["converged"] and conv_o
+            assert abs(stats[b]["iters"] - it_o) <= 1, (env, b, stats[b]["iters"], it_o)
+            assert relerr(x[b], xo) <= 1e-9, (env, relerr(x[b], xo))
+
+
+def test_pcg_variable_coefficients_standard_path(torch_cuda):
+    """PCG on a symmetric variable-coefficient operator is not SPD in general;
+    with d₊ = d₋ = const fields given explicitly the standard fused path (not
+    the sine path, which needs constants) runs and matches the oracle."""
+    p = W.config(3, n=63)
+    p.dp_field = np.full(p.N, 1.0)
+    p.dm_field = np.full(p.N, 1.0)
+    s = oracle_system(p)
+    st, stats, x, _ = gpu_solve(torch_cuda, p, "pcg")
+    (xo, it_o, conv_o, _), = oracle_solve(p, s, "pcg")
+    assert abs(stats[0]["iters"] - it_o) <= 1
+    assert relerr(x[0], xo) <= 1e-9
+
+
+def test_batch_rhs_are_independent_and_deterministic(torch_cuda):
+    """Per-RHS grids and per-RHS fixed-order reductions: a batch-3 solve equals
+    the three single-RHS solves bitwise, and repeating a solve is bitwise
+    identical (S:L420)."""
+    from paper_1912_13304_b200 import fde
+    for cfg, n, solver in ((5, 255, "pcg"), (4, 127, "gmres")):
+        p = W.config(cfg, n=n, batch=3)
+        _, _, x3, _ = gpu_solve(torch_cuda, p, solver)
+        _, _, x3b, _ = gpu_solve(torch_cuda, p, solver)
+        assert np.array_equal(x3, x3b)
+        for b in range(3):
+            q = W.config(cfg, n=n, batch=1)
+            q.rhs = p.rhs[b:b + 1].copy()
+            _, _, x1, _ = gpu_solve(torch_cuda, q, solver)
+            assert np.array_equal(x1[0], x3[b]), (cfg, b)
+
+
+def test_not_converged_status_keeps_last_iterate(torch_cuda):
+    from paper_1912_13304_b200 import fde
+    p = W.config(5, n=255)
+    h = fde.Fde.from_problem(p)
+    b = torch_cuda.from_numpy(p.rhs.copy()).cuda()
+    x = torch_cuda.zeros_like(b)
+    st, stats = h.pcg(b, x, 1e-10, 5)
+    assert st == fde.FDE_ERR_NOT_CONVERGED and stats[0]["iters"] == 5 and not stats[0]["converged"]
+    assert np.all(np.isfinite(x.cpu().numpy())) and float(x.abs().sum()) > 0
+    h.close()
+
+
+def test_profile_abis_report_every_kernel(torch_cuda):
+    """fde_profile_unit / fde_profile_solve (bench.py's roofline leg) name and
+    time every kernel of the unit and of one loop body."""
+    from paper_1912_13304_b200 import fde
+    p = W.config(5, n=255)
+    h = fde.Fde.from_problem(p)
+    b = torch_cuda.from_numpy(p.rhs.copy()).cuda()
+    y, z = torch_cuda.empty_like(b), torch_cuda.empty_like(b)
+    unit = h.profile_unit(b, y, z, reps=3)
+    assert [nm for nm, _ in unit] == ["toeplitz_rows", "toeplitz_cols", "dst_rows", "tau_cols", "dst_rows"]
+    assert all(us > 0 for _, us in unit)
+    x = torch_cuda.zeros_like(b)
+    live, stats = h.profile_solve(b, x, "pcg", 1e-10, 4)
+    assert [nm for nm, _ in live] == ["sine_op_rows", "sine_op_cols", "sine_xr"]
+    assert stats[0]["iters"] == 4
+    h.close()
+    p = W.config(4, n=127)
+    h = fde.Fde.from_problem(p)
+    b = torch_cuda.from_numpy(p.rhs.copy()).cuda()
+    x = torch_cuda.zeros_like(b)
+    live, _ = h.profile_solve(b, x, "gmres", 1e-10, 30, restart=5)
+    names = [nm for nm, _ in live]
+    assert names.count("gm_upd_norm") == 5 and "toeplitz_rows_var" in names
+    h.close()
