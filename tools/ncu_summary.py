@@ -76,15 +76,22 @@ def _scale(u):
 
 def _short(name):
     """ncu kernel name -> the library's launch name (fde_profile_unit names)."""
-    n = name.split("(")[0]
+    n = name.split("(")[0].replace("void ", "").replace("fde::", "")
     if "k_toeplitz_lines" in n:
         t = n.split("<")[1].split(">")[0].split(",")
         col, var = t[2].strip() == "1", t[3].strip() == "1"
         return ("toeplitz_cols" if col else "toeplitz_rows") + ("_var" if var else "")
     if "k_tau_lines" in n:
         return "tau_cols" if n.split("<")[1].split(",")[2].strip() == "1" else "tau_rows"
-    if "k_dst_lines" in n:
-        return "dst_cols" if n.split("<")[1].split(",")[2].strip() == "1" else "dst_rows"
+    if "k_dstm_lines" in n:
+        t = [v.strip() for v in n.split("<")[1].split(">")[0].split(",")]
+        col, tau = t[2] == "1", t[4] == "1"
+        return ("tau" if tau else "dst") + ("_cols" if col else "_rows")
+    if "k_sineop_lines" in n:
+        mode = n.split("<")[1].split(">")[0].split(",")[3].strip()
+        return {"0": "sine_op_rows", "1": "sine_op_cols", "2": "sine_op_1d"}[mode]
+    if "k_sine_xr" in n:
+        return "sine_xr"
     return n
 
 
