@@ -20,6 +20,8 @@
  *   FDE_PREC_TAU_D    P = τ(F)·D          (the form the paper's tables measure;
  *                                          DESIGN.md reading R6)
  *   FDE_PREC_TAU_DSYM P = D^{1/2} τ(F) D^{1/2}   (P:L313 as printed)
+ *   FDE_PREC_TILDE    P̃ = S diag(D_j·F(θ_j)) S  (1D only; the alternative of P:L606,
+ *                                          Table 2; reading R7)
  *   D = (D₊+D₋)/2 in 1D, (D₊+D₋+E₊+E₋)/4 in 2D.
  *
  * Layout: every vector is fp64, C-contiguous, x-fastest: element
@@ -65,7 +67,8 @@ typedef enum {
   FDE_PREC_NONE = 0,
   FDE_PREC_TAU = 1,
   FDE_PREC_TAU_D = 2,
-  FDE_PREC_TAU_DSYM = 3
+  FDE_PREC_TAU_DSYM = 3,
+  FDE_PREC_TILDE = 4
 } fde_prec;
 
 typedef struct {
@@ -82,7 +85,7 @@ typedef struct {
   const double* dm_field;
   const double* ep_field;
   const double* em_field;
-  int32_t prec;     /* fde_prec */
+  int32_t prec;     /* fde_prec (FDE_PREC_TILDE needs dims == 1) */
   double cx, cy;    /* τ weights; <= 0 selects: TAU -> mean((d₊+d₋)/2), mean((e₊+e₋)/2)
                        (R12); TAU_D/TAU_DSYM -> 1 */
   double ywt;       /* weight of the 2D y-term (the paper's s/r); <= 0 -> 1 */
@@ -113,7 +116,8 @@ fde_status fde_tau_apply(fde_handle h, const double* r, double* z);
 
 /* Preconditioned CG (x0 = 0; stop when ‖r_k‖ <= rtol‖b‖).
  * Requires an SPD operator and preconditioner (d₊ = d₋, e₊ = e₋ constant,
- * prec TAU or NONE). st: array of `batch` stats (may be NULL). Returns the
+ * prec TAU, TILDE or NONE; TAU with constant coefficients runs in the sine
+ * basis). st: array of `batch` stats (may be NULL). Returns the
  * worst per-RHS status. */
 fde_status fde_pcg(fde_handle h, const double* b, double* x, double rtol, int32_t maxit, fde_stats* st);
 

@@ -23,6 +23,7 @@
 #include "krylov_kernels.cuh"
 #include "line_kernels.cuh"
 #include "sine_kernels.cuh"
+#include "dense_kernels.cuh"
 
 using namespace fde;
 
@@ -53,7 +54,8 @@ struct FdeFail {
 #define FDE_KRM 3
 #endif
 constexpr int KMIN = 6, KMAX = 13, KR = FDE_KR;  // log2 points per thread in the FFT engine (length-L FFTs)
-constexpr int KRM = FDE_KRM;                      // same for the length-m FFTs of the DST kernels
+constexpr int KRM = FDE_KRM;
+constexpr int DENSE_MAX = 2048;                   // largest n of the direct path                      // same for the length-m FFTs of the DST kernels
 
 // ------------------------------------------------------------------ host maths
 std::vector<double> grunwald(double alpha, int K) {  // g_k = (-1)^k C(α,k)
@@ -222,6 +224,8 @@ struct fde_handle_s {
   long long launches = 0;
 
   // tables
+  bool dense = false;                 // direct path (dense_kernels.cuh): n+1 not a supported power of two
+  double *coef_x = nullptr, *coef_y = nullptr, *sint = nullptr;
   double2* tw = nullptr;
   double2* twp = nullptr;
   double2* twpm = nullptr;
@@ -449,9 +453,112 @@ void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const dou
   }
 }
 
+// ------------------------------------------------------- direct path (dense)
+void launch_dense(fde_handle h, bool col, int mode, const LineArgs& a, const DenseArgs& dd) {
+  const dim3 grid(a.nlines, h->batch);
+  const int smem = (int)((2 * h->n + 2 * h->m + 8) * sizeof(double));
+  const char* nm = mode == 0 ? (col ? "dense_toeplitz_cols" : "dense_toeplitz_rows")
+                             : (mode == 1 ? (col ? "dense_dst_cols" : "dense_dst_rows") : (col ? "dense_tau_cols" : "dense_tau_rows"));
+  launch_named(h, nm, [&] {
+    if (col) {
+      if (mode == 0) k_dense_lines<true, 0><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
+      else if (mode == 1) k_dense_lines<true, 1><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
+      else k_dense_lines<true, 2><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
+    } else {
+      if (mode == 0) k_dense_lines<false, 0><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
+      else if (mode == 1) k_dense_lines<false, 1><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
+      else k_dense_lines<false, 2><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
+    }
+  });
+}
+
+void dense_matvec(fde_handle h, const double* x, double* y, const int* gate, const KryFuse* kf) {
+  const double ywt = h->d.ywt > 0.0 ? h->d.ywt : 1.0;
+  KryFuse k0{}, k1{};
+  if (kf) {
+    k0 = *kf;
+    k1 = *kf;
+    if (h->dims == 2) {
+      k0.mode &= (KM_PUPD | KM_GATE);
+      k1.mode &= (KM_PQ | KM_GATE);
+    }
+  }
+  LineArgs a = base_args(h);
+  a.gate = gate;
+  a.kf = k0;
+  a.x = x;
+  a.y = h->dims == 1 ? y : h->wx;
+  a.nu = h->d.nu;
+  a.nlines = h->dims == 1 ? 1 : h->n;
+  a.cP = h->var_x ? h->cP_x : nullptr;
+  a.cM = h->var_x ? h->cM_x : nullptr;
+  launch_dense(h, false, 0, a, DenseArgs{h->coef_x, nullptr, h->d.dp, h->d.dm});
+  if (h->dims == 1) return;
+  LineArgs b = base_args(h);
+  b.gate = gate;
+  b.kf = k1;
+  b.x = (kf && (kf->mode & KM_PUPD)) ? kf->p : x;
+  b.yin = h->wx;
+  b.y = y;
+  b.nlines = h->n;
+  b.cP = h->var_y ? h->cP_y : nullptr;
+  b.cM = h->var_y ? h->cM_y : nullptr;
+  launch_dense(h, true, 0, b, DenseArgs{h->coef_y, nullptr, ywt * h->d.ep, ywt * h->d.em});
+}
+
+void dense_tau(fde_handle h, const double* r, double* z, const int* gate, const KryFuse* kf) {
+  KryFuse kpre{}, kmid{}, kpost{};
+  if (kf) {
+    kpre = kmid = kpost = *kf;
+    if (h->dims == 2) {
+      kpre.mode &= (KM_XR | KM_GATE);
+      kmid.mode &= KM_GATE;
+      kpost.mode &= (KM_RZ | KM_GATE);
+    }
+  }
+  const DenseArgs dd{nullptr, h->sint, 0.0, 0.0};
+  LineArgs a = base_args(h);
+  a.gate = gate;
+  a.kf = kpre;
+  if (h->dims == 1) {
+    a.x = r;
+    a.y = z;
+    a.nlines = 1;
+    a.invF = h->invF;
+    a.dpre = h->dpre;
+    a.dpost = h->dpost;
+    launch_dense(h, false, 2, a, dd);
+    return;
+  }
+  a.nlines = h->n;
+  a.x = r;
+  a.y = h->t1;
+  a.dpre = h->dpre;
+  launch_dense(h, false, 1, a, dd);
+  LineArgs b = base_args(h);
+  b.gate = gate;
+  b.kf = kmid;
+  b.nlines = h->n;
+  b.x = h->t1;
+  b.y = h->t2;
+  b.Fx = h->Fx;
+  b.Fy = h->Fy;
+  b.fscale = h->fscale;
+  launch_dense(h, true, 2, b, dd);
+  LineArgs c = base_args(h);
+  c.gate = gate;
+  c.kf = kpost;
+  c.nlines = h->n;
+  c.x = h->t2;
+  c.y = z;
+  c.dpost = h->dpost;
+  launch_dense(h, false, 1, c, dd);
+}
+
 // y = A x (a1). With kf (fused PCG): x is z, the row pass forms p = z + βp
 // (KM_PUPD) and the pass completing y = A p accumulates p·y (KM_PQ).
 void op_matvec(fde_handle h, const double* x, double* y, const int* gate, const KryFuse* kf = nullptr) {
+  if (h->dense) return dense_matvec(h, x, y, gate, kf);
   KryFuse k0{}, k1{};
   if (kf) {
     k0 = *kf;
@@ -497,6 +604,7 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate, const Kry
     }
     return;
   }
+  if (h->dense) return dense_tau(h, r, z, gate, kf);
   LineArgs a = base_args(h);
   a.gate = gate;
   if (kf) a.kf = kpre;
@@ -547,12 +655,13 @@ void build(fde_handle h, const fde_desc* d) {
   h->batch = d->batch;
   h->N = d->dims == 1 ? n : n * n;
   const int Km = ilog2_exact(h->m);
-  if (Km < 0 || Km + 1 < KMIN || Km + 1 > KMAX)
-    throw FdeFail{FDE_ERR_UNSUPPORTED, "hot path needs n+1 a power of two with 32 <= n+1 <= 4096"};
-  h->K = Km + 1;
+  h->dense = Km < 0 || Km + 1 < KMIN || Km + 1 > KMAX;
+  if (h->dense && n > DENSE_MAX)
+    throw FdeFail{FDE_ERR_UNSUPPORTED, "n+1 must be a power of two in [32, 4096] (FFT path) or n <= 2048 (direct path)"};
+  h->K = h->dense ? 0 : Km + 1;
   h->L = 2 * h->m;
   const int L = h->L, m = h->m, N = h->N;
-  FDE_SWITCH_K(h->K, (init_kernel_attrs<KK>()));
+  if (!h->dense) { FDE_SWITCH_K(h->K, (init_kernel_attrs<KK>())); }
 
   // fields to host (for D, means and the combined coefficient fields)
   auto field = [&](const double* f, double c) {
@@ -573,17 +682,42 @@ void build(fde_handle h, const fde_desc* d) {
   h->var_y = two && (d->ep_field || d->em_field);
   const double ywt = d->ywt > 0.0 ? d->ywt : 1.0;
 
-  // twiddles: quarter table exp(-2πi r/L), r < L/4 (fft_engine.cuh tw_lookup)
-  std::vector<double2> tw(L / 4);
-  for (int e = 0; e < L / 4; ++e) { auto z = root_of_unity(e, L); tw[e] = make_double2(z.real(), z.imag()); }
-  h->tw = h->upload(tw);
-  // per-pass twiddle tables of the length-L (Toeplitz) and length-m (DST) FFTs
-  h->twp = h->upload(pass_twiddles_host(h->K, KR));
-  h->twpm = h->upload(pass_twiddles_host(h->K - 1, KRM));
-  {
+  if (!h->dense) {
+    // per-pass twiddle tables of the length-L (Toeplitz) and length-m (DST) FFTs
+    h->twp = h->upload(pass_twiddles_host(h->K, KR));
+    h->twpm = h->upload(pass_twiddles_host(h->K - 1, KRM));
     std::vector<double> sv(m);
     for (int j = 0; j < m; ++j) sv[j] = std::sin(M_PI * (double)std::min(j, m - j) / (double)m);  // sin(πj/m)
     h->sinm = h->upload(sv);
+  } else {
+    // direct path (dense_kernels.cuh): stencil coefficients and sin(π r/m), r < 2m
+    h->coef_x = h->upload(stencil_coeffs(d->alpha, n, d->stencil));
+    if (two) h->coef_y = h->upload(stencil_coeffs(d->beta, n, d->stencil));
+    std::vector<double> st(2 * m);
+    for (int r = 0; r < 2 * m; ++r) {
+      const int rr = r % m, red = std::min(rr, m - rr);
+      st[r] = (r < m ? 1.0 : -1.0) * std::sin(M_PI * (double)red / (double)m);
+    }
+    h->sint = h->upload(st);
+    auto fields = [&](bool var, double wgt, double*& cPf, double*& cMf, const std::vector<double>& fp,
+                      const std::vector<double>& fm) {
+      if (!var) return;
+      std::vector<double> pv(N), qv(N);
+      for (int i = 0; i < N; ++i) { pv[i] = wgt * (fp[i] + fm[i]); qv[i] = wgt * (fp[i] - fm[i]); }
+      cPf = h->upload(pv);
+      cMf = h->upload(qv);
+    };
+    fields(h->var_x, 1.0, h->cP_x, h->cM_x, dp, dm);
+    if (two) fields(h->var_y, ywt, h->cP_y, h->cM_y, ep, em);
+    const int smem = (int)((2 * n + 2 * m + 8) * sizeof(double));
+    if (smem > 48 * 1024) {
+      FDE_CUDA(cudaFuncSetAttribute(k_dense_lines<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      FDE_CUDA(cudaFuncSetAttribute(k_dense_lines<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      FDE_CUDA(cudaFuncSetAttribute(k_dense_lines<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      FDE_CUDA(cudaFuncSetAttribute(k_dense_lines<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      FDE_CUDA(cudaFuncSetAttribute(k_dense_lines<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      FDE_CUDA(cudaFuncSetAttribute(k_dense_lines<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
   }
 
   // circulant eigenvalues λ = DFT_L(c), c = first column of the embedding
@@ -637,8 +771,10 @@ void build(fde_handle h, const fde_desc* d) {
       cMf = h->upload(q);
     }
   };
-  make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, d->nu, h->mu_x, h->mus_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm);
-  if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, 0.0, h->mu_y, h->mus_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em);
+  if (!h->dense) {
+    make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, d->nu, h->mu_x, h->mus_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm);
+    if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, 0.0, h->mu_y, h->mus_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em);
+  }
 
   // preconditioner tables
   const int prec = d->prec;
@@ -672,6 +808,13 @@ void build(fde_handle h, const fde_desc* d) {
     if (!two) {
       std::vector<double> inv(n);
       for (int j = 0; j < n; ++j) inv[j] = 1.0 / (cx * Fa[j]) / (2.0 * m);
+      if (prec == FDE_PREC_TILDE) {  // P̃ = S diag(D_j F_j) S (R7): node j paired with frequency j
+        for (int j = 0; j < n; ++j) {
+          const double Dj = 0.5 * (dp[j] + dm[j]);
+          if (!(Dj > 0.0)) throw FdeFail{FDE_ERR_SINGULAR, "D has a zero entry (common zero of the coefficients)"};
+          inv[j] /= Dj;
+        }
+      }
       h->invF = h->upload(inv);
       std::vector<double> fx(n);
       for (int j = 0; j < n; ++j) fx[j] = cx * Fa[j];
@@ -737,7 +880,8 @@ void validate(const fde_desc* d) {
   coef(d->dp);
   coef(d->dm);
   if (d->dims == 2) { coef(d->ep); coef(d->em); }
-  if (d->prec < FDE_PREC_NONE || d->prec > FDE_PREC_TAU_DSYM) bad("unknown prec kind");
+  if (d->prec < FDE_PREC_NONE || d->prec > FDE_PREC_TILDE) bad("unknown prec kind");
+  if (d->prec == FDE_PREC_TILDE && d->dims != 1) bad("FDE_PREC_TILDE is defined in 1D only (P:L606)");
   if (!std::isfinite(d->cx) || !std::isfinite(d->cy) || !std::isfinite(d->ywt)) bad("cx, cy, ywt must be finite");
   if ((long long)d->n * (d->dims == 2 ? d->n : 1) * d->batch > (1LL << 31)) bad("problem too large");
 }
@@ -933,7 +1077,7 @@ void pcg_iteration(fde_handle h, const VecArgs& va) {
 // Constant coefficients with the τ preconditioner: PCG on x̂ = (S⊗S)x
 // (sine_kernels.cuh). Per iteration: 2D = row operator, column operator (+p·q),
 // vector step; 1D = operator, vector step.
-bool sine_pcg_ok(fde_handle h) { return h->d.prec == FDE_PREC_TAU && !h->var_x && !h->var_y; }
+bool sine_pcg_ok(fde_handle h) { return !h->dense && h->d.prec == FDE_PREC_TAU && !h->var_x && !h->var_y; }
 
 KryFuse make_kf(fde_handle h, double rtol, int maxit) {
   KryFuse kf{};
@@ -1258,7 +1402,7 @@ fde_status fde_pcg(fde_handle h, const double* b, double* x, double rtol, int32_
   if (!h) return FDE_ERR_INVALID_ARG;
   if (!b || !x || (const void*)b == (const void*)x) { h->err = "b/x NULL or aliased"; return FDE_ERR_INVALID_ARG; }
   if (!(rtol > 0.0) || maxit < 1) { h->err = "rtol must be > 0 and maxit >= 1"; return FDE_ERR_INVALID_ARG; }
-  if (h->d.prec != FDE_PREC_NONE && h->d.prec != FDE_PREC_TAU) {
+  if (h->d.prec != FDE_PREC_NONE && h->d.prec != FDE_PREC_TAU && h->d.prec != FDE_PREC_TILDE) {
     h->err = "PCG needs a symmetric preconditioner (NONE or TAU)";
     return FDE_ERR_INVALID_ARG;
   }

@@ -54,15 +54,17 @@ def _create(**kw):
 @pytest.mark.parametrize("kw", [
     dict(alpha=1.0), dict(alpha=2.0), dict(alpha=float("nan")), dict(dims=2, beta=2.5), dict(dims=3),
     dict(n=0), dict(batch=0), dict(batch=9), dict(nu=-1.0), dict(nu=float("inf")), dict(dp=-1.0),
-    dict(prec=7), dict(stencil=3), dict(cx=float("nan")),
+    dict(prec=7), dict(stencil=3), dict(cx=float("nan")), dict(dims=2, prec=4),
 ])
 def test_create_rejects_invalid(kw):
     assert _create(**kw) == 1   # FDE_ERR_INVALID_ARG, decided before any CUDA call
 
 
-@pytest.mark.parametrize("n", [100, 126, 8191, 15])
+@pytest.mark.parametrize("n", [8191, 5000, 2049, 16383])
 def test_create_unsupported_sizes(n):
-    assert _create(n=n) == 2    # FDE_ERR_UNSUPPORTED (n+1 not a power of two in [32, 4096])
+    # FDE_ERR_UNSUPPORTED: n+1 not a power of two in [32, 4096] (FFT path) and
+    # n > 2048 (direct path); decided before any CUDA call
+    assert _create(n=n) == 2
 
 
 def test_null_handle_and_args():

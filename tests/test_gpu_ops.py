@@ -204,3 +204,34 @@ def test_determinism(torch_cuda):
     b = run_op(torch_cuda, h, "tau_apply", p.rhs)
     assert np.array_equal(a, b)
     h.close()
+
+
+# direct path (dense_kernels.cuh): n+1 not a power of two or n+1 < 32
+DENSE_CASES = [
+    (1, 15, 1, W.PREC_TAU), (1, 100, 2, W.PREC_TAU), (2, 200, 1, W.PREC_TAU_D), (2, 99, 2, W.PREC_TAU_DSYM),
+    (3, 16, 1, W.PREC_TAU), (3, 40, 2, W.PREC_TAU), (4, 33, 1, W.PREC_TAU), (4, 64, 2, W.PREC_TAU_D),
+    (4, 17, 1, W.PREC_TAU_DSYM), (5, 128, 3, W.PREC_TAU),
+]
+
+
+@pytest.mark.parametrize("cfg,n,batch,prec", DENSE_CASES, ids=lambda v: str(v))
+def test_direct_path_matvec_and_tau_parity(torch_cuda, cfg, n, batch, prec):
+    test_matvec_and_tau_parity(torch_cuda, cfg, n, batch, prec)
+
+
+@pytest.mark.parametrize("n", [16, 33])
+def test_direct_path_wsgd_example2_operators(torch_cuda, n):
+    """The paper's 2D system at its own sizes: WSGD
+    stencil, Crank-Nicolson weights ν = 1/r and ywt = s/r, Example 2 fields
+    (P:L654-655), P = τ(q_α + (s/r) q_β)·D_N (R6, R15)."""
+    from paper_1912_13304_b200 import fde
+    ex = W.example2(1.8, 1.6, n)
+    s, inv_r, s_over_r = O.example2_matrices(ex, 1.8, 1.6, n)
+    h = fde.Fde(n, 2, 1.8, 1.6, nu=inv_r, dp_field=ex["dp"], dm_field=ex["dm"], ep_field=ex["ep"],
+                em_field=ex["em"], prec=W.PREC_TAU_D, cx=1.0, cy=s_over_r, ywt=s_over_r, stencil=2)
+    x = np.random.default_rng(5).standard_normal((1, n * n))
+    y = run_op(torch_cuda, h, "matvec", x)
+    z = run_op(torch_cuda, h, "tau_apply", x)
+    assert relerr(y[0], s.matvec(x[0])) <= TOL
+    assert relerr(z[0], s.prec_solve(x[0], O.PREC_TAU_D, 1.0, s_over_r)) <= TOL
+    h.close()
