@@ -24,6 +24,7 @@ constexpr int DENSE_THREADS = 128;
 // MODE 2: τ core DST -> ×s -> DST (1D rows: invF; 2D columns: fscale/(Fx_l + Fy_k); hooks XR, RZ)
 template <bool COL, int MODE>
 __global__ void __launch_bounds__(DENSE_THREADS) k_dense_lines(LineArgs a, DenseArgs d) {
+  FDE_PDL_ENTRY();
   extern __shared__ double dsm[];
   if (a.gate && *a.gate == 0) return;
   if (kry_skip(a)) return;

@@ -129,6 +129,7 @@ __device__ __forceinline__ void dstm_pre_smem(double2 (&v)[G::R], const double2*
 template <int KM, int k, bool COL, int FPC, bool TAU>
 __global__ void __launch_bounds__(FPC * (1 << (KM - k)), min_blocks_for(FPC * (1 << (KM - k))))
 k_dstm_lines(LineArgs a) {
+  FDE_PDL_ENTRY();
   using G = FftGeom<KM, k>;
   using M = LineMap<G, COL, FPC>;
   constexpr int m = G::L, P = G::P, R = G::R, C = R / 2;

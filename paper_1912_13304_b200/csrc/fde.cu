@@ -47,6 +47,27 @@ struct FdeFail {
                     std::string(#call) + ": " + cudaGetErrorString(e_)};                \
   } while (0)
 
+// Every kernel launch goes through cudaLaunchKernelEx; with FDE_PDL=1 it
+// carries programmatic stream serialisation (PDL, see FDE_PDL_ENTRY). Off by
+// default: measured on the B200 it did not help (cfg 5 n=1023 11.2k vs 11.5k
+// PCG it/s, cfg 3 69.6 vs 51.5 µs/iteration) — the early-launched dependent
+// CTAs hold SM slots while they wait.
+bool g_pdl = false;
+template <typename... KArgs, typename... Args>
+void launch_k(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FDE_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 #ifndef FDE_KR
 #define FDE_KR 4
 #endif
@@ -334,7 +355,7 @@ void launch_toep_k(fde_handle h, const LineArgs& a) {
   const int npairs = (a.nlines + 1) / 2;
   const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
   launch_named(h, COL ? (VAR ? "toeplitz_cols_var" : "toeplitz_cols") : (VAR ? "toeplitz_rows_var" : "toeplitz_rows"),
-               [&] { kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a); });
+               [&] { launch_k(h->st, kern, grid, C::THREADS, C::SMEM, a); });
 }
 template <int KM, bool COL, bool TAU>
 void launch_dstm_k(fde_handle h, const LineArgs& a) {
@@ -343,7 +364,7 @@ void launch_dstm_k(fde_handle h, const LineArgs& a) {
   const int npairs = (a.nlines + 1) / 2;
   const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
   launch_named(h, TAU ? (COL ? "tau_cols" : "tau_rows") : (COL ? "dst_cols" : "dst_rows"),
-               [&] { kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a); });
+               [&] { launch_k(h->st, kern, grid, C::THREADS, C::SMEM, a); });
 }
 
 template <int KM, bool COL, int MODE>
@@ -358,7 +379,7 @@ void launch_sineop_k(fde_handle h, const LineArgs& a) {
   const int npairs = (a.nlines + 1) / 2;
   const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
   launch_named(h, MODE == 0 ? "sine_op_rows" : (MODE == 1 ? "sine_op_cols" : "sine_op_1d"),
-               [&] { kern<<<grid, C::THREADS, C::SMEM, h->st>>>(a); });
+               [&] { launch_k(h->st, kern, grid, C::THREADS, C::SMEM, a); });
 }
 
 #define FDE_SWITCH_K(K, CALL)                                           \
@@ -461,13 +482,13 @@ void launch_dense(fde_handle h, bool col, int mode, const LineArgs& a, const Den
                              : (mode == 1 ? (col ? "dense_dst_cols" : "dense_dst_rows") : (col ? "dense_tau_cols" : "dense_tau_rows"));
   launch_named(h, nm, [&] {
     if (col) {
-      if (mode == 0) k_dense_lines<true, 0><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
-      else if (mode == 1) k_dense_lines<true, 1><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
-      else k_dense_lines<true, 2><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
+      if (mode == 0) launch_k(h->st, k_dense_lines<true, 0>, grid, DENSE_THREADS, smem, a, dd);
+      else if (mode == 1) launch_k(h->st, k_dense_lines<true, 1>, grid, DENSE_THREADS, smem, a, dd);
+      else launch_k(h->st, k_dense_lines<true, 2>, grid, DENSE_THREADS, smem, a, dd);
     } else {
-      if (mode == 0) k_dense_lines<false, 0><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
-      else if (mode == 1) k_dense_lines<false, 1><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
-      else k_dense_lines<false, 2><<<grid, DENSE_THREADS, smem, h->st>>>(a, dd);
+      if (mode == 0) launch_k(h->st, k_dense_lines<false, 0>, grid, DENSE_THREADS, smem, a, dd);
+      else if (mode == 1) launch_k(h->st, k_dense_lines<false, 1>, grid, DENSE_THREADS, smem, a, dd);
+      else launch_k(h->st, k_dense_lines<false, 2>, grid, DENSE_THREADS, smem, a, dd);
     }
   });
 }
@@ -579,7 +600,7 @@ void op_matvec(fde_handle h, const double* x, double* y, const int* gate, const 
 
 void op_copy(fde_handle h, const double* src, double* dst) {
   const long long n = (long long)h->vec_elems();
-  launch_named(h, "copy", [&] { k_copy<<<592, 256, 0, h->st>>>(src, dst, n); });
+  launch_named(h, "copy", [&] { launch_k(h->st, k_copy, 592, 256, 0, src, dst, n); });
 }
 
 // z = P⁻¹ r (a2). With kf (fused PCG): the first kernel forms r -= αq,
@@ -598,7 +619,7 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate, const Kry
     if (kf) {
       const KryFuse k = *kf;
       const int N = h->N;
-      launch_named(h, "pcg_xrz_none", [&] { k_pcg_xrz_none<<<dim3(296, h->batch), 256, 0, h->st>>>(k, N, z); });
+      launch_named(h, "pcg_xrz_none", [&] { launch_k(h->st, k_pcg_xrz_none, dim3(296, h->batch), 256, 0, k, N, z); });
     } else {
       op_copy(h, r, z);
     }
@@ -859,6 +880,8 @@ void build(fde_handle h, const fde_desc* d) {
     h->force_standard_pcg = e && std::strcmp(e, "standard") == 0;
     const char* g = std::getenv("FDE_GRAPH");
     h->no_graph = g && std::strcmp(g, "0") == 0;
+    const char* pd = std::getenv("FDE_PDL");
+    g_pdl = pd && std::strcmp(pd, "1") == 0;
   }
   h->part = h->dalloc<double>((size_t)h->batch * (MAX_RESTART + 1) * RED_BLOCKS);
   FDE_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->st));
@@ -945,6 +968,7 @@ VecArgs vec_args(fde_handle h, double rtol, int maxit, int restart, int left) {
 }
 
 __global__ void k_reset_counters(Counters* c, SolveState* s, int batch) {
+  FDE_PDL_ENTRY();
   if (threadIdx.x == 0) {
     c->active = batch;
     c->unfinished = batch;
@@ -965,6 +989,7 @@ __global__ void k_reset_counters(Counters* c, SolveState* s, int batch) {
 
 // measurement: every RHS iterating again (fde_profile_solve)
 __global__ void k_reactivate(Counters* c, SolveState* s, int batch) {
+  FDE_PDL_ENTRY();
   if (threadIdx.x == 0) {
     c->active = batch;
     c->unfinished = batch;
@@ -1020,7 +1045,7 @@ int build_while_graph(fde_handle h, cudaGraphExec_t* out, int maxloops, F&& body
   try {
     FDE_CUDA(cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     body();
-    k_loop_ctrl<<<1, 1, 0, cs>>>(ch, h->ctr, maxloops);
+    launch_k(cs, k_loop_ctrl, 1, 1, 0, ch, h->ctr, maxloops);
     FDE_CUDA(cudaGetLastError());
     cudaGraph_t captured;
     FDE_CUDA(cudaStreamEndCapture(cs, &captured));
@@ -1154,14 +1179,14 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
   const double* Fy = h->dims == 2 ? h->Fy : nullptr;
   const int n = h->n, dims = h->dims;
   const int gx = dims == 2 ? std::min(n, KPMAX) : 64;
-  launch_named(h, "sine_xr", [&] { k_sine_xr<<<dim3(gx, h->batch), 256, 0, h->st>>>(kv, n, dims, Fx, Fy); });
+  launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr, dim3(gx, h->batch), 256, 0, kv, n, dims, Fx, Fy); });
 }
 
 fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, int maxit, fde_stats* st) {
   ensure_krylov(h, 0);
   bool bh = false;
   const double* bd = stage_in(h, b, h->hin, bh);
-  k_reset_counters<<<1, 32, 0, h->st>>>(h->ctr, h->sst, h->batch);
+  launch_k(h->st, k_reset_counters, 1, 32, 0, h->ctr, h->sst, h->batch);
   h->launches++;
   op_dst_all(h, bd, h->kr, 0.0);  // r̂ = b̂ (unnormalised)
   KryFuse kf = make_kf(h, rtol, maxit);
@@ -1169,7 +1194,7 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   const double* Fy = h->dims == 2 ? h->Fy : nullptr;
   const int n = h->n, dims = h->dims;
   const int gx = dims == 2 ? std::min(n, KPMAX) : 64;
-  launch_named(h, "sine_init", [&] { k_sine_init<<<dim3(gx, h->batch), 256, 0, h->st>>>(kf, n, dims, Fx, Fy); });
+  launch_named(h, "sine_init", [&] { launch_k(h->st, k_sine_init, dim3(gx, h->batch), 256, 0, kf, n, dims, Fx, Fy); });
   if (!h->no_graph && (!h->g_pcg || h->g_rtol != rtol || h->g_maxit != maxit)) {
     if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
     h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { sine_iteration(h, rtol, maxit); });
@@ -1200,11 +1225,11 @@ fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int ma
   bool bh = false;
   const double* bd = stage_in(h, b, h->hin, bh);
   const VecArgs va = vec_args(h, rtol, maxit, 0, 0);
-  k_reset_counters<<<1, 32, 0, h->st>>>(h->ctr, h->sst, h->batch);
-  k_pcg_init<<<VGRID, RED_THREADS, 0, h->st>>>(va, bd, h->kx, h->kr);
+  launch_k(h->st, k_reset_counters, 1, 32, 0, h->ctr, h->sst, h->batch);
+  launch_k(h->st, k_pcg_init, VGRID, RED_THREADS, 0, va, bd, h->kx, h->kr);
   h->launches += 2;
   op_tau(h, h->kr, h->kz, nullptr);
-  k_pcg_init2<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kr, h->kz, h->kp);
+  launch_k(h->st, k_pcg_init2, VGRID, RED_THREADS, 0, va, h->kr, h->kz, h->kp);
   h->launches++;
   FDE_CUDA(cudaGetLastError());
 
@@ -1233,7 +1258,7 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
   const int* gU = &h->ctr->unfinished;
   const size_t vs = h->vec_elems();
   double* V = h->V;
-  launch_named(h, "gm_scale", [&] { k_gm_scale<<<VGRID, RED_THREADS, 0, h->st>>>(va, V); });
+  launch_named(h, "gm_scale", [&] { launch_k(h->st, k_gm_scale, VGRID, RED_THREADS, 0, va, V); });
   for (int j = 0; j < restart; ++j) {
     double* Vj = V + (size_t)j * vs;
     double* Vn = V + (size_t)(j + 1) * vs;
@@ -1244,31 +1269,31 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
       op_matvec(h, Vj, h->kq, gA);
       op_tau(h, h->kq, Vn, gA);
     }
-    launch_named(h, "gm_mdot", [&] { k_gm_mdot<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j); });
+    launch_named(h, "gm_mdot", [&] { launch_k(h->st, k_gm_mdot, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
     if (j < 32)
-      launch_named(h, "gm_upd_mdot", [&] { k_gm_upd_mdot32<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j); });
+      launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k_gm_upd_mdot32, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
     else
-      launch_named(h, "gm_upd_mdot", [&] { k_gm_upd_mdot<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j); });
-    launch_named(h, "gm_upd_norm", [&] { k_gm_upd_norm<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, Vn, j); });
-    if (j + 1 < restart) launch_named(h, "gm_scale", [&] { k_gm_scale<<<VGRID, RED_THREADS, 0, h->st>>>(va, Vn); });
+      launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k_gm_upd_mdot, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+    launch_named(h, "gm_upd_norm", [&] { launch_k(h->st, k_gm_upd_norm, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+    if (j + 1 < restart) launch_named(h, "gm_scale", [&] { launch_k(h->st, k_gm_scale, VGRID, RED_THREADS, 0, va, Vn); });
   }
   // end of cycle: x += P⁻¹(V y) (right) or V y (left); restart residual
-  launch_named(h, "gm_lincomb", [&] { k_gm_lincomb<<<VGRID, RED_THREADS, 0, h->st>>>(va, V, vs, h->kp); });
+  launch_named(h, "gm_lincomb", [&] { launch_k(h->st, k_gm_lincomb, VGRID, RED_THREADS, 0, va, V, vs, h->kp); });
   if (!left) {
     op_tau(h, h->kp, h->kz, gU);
-    k_gm_xupd<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kz, h->kx);
+    launch_k(h->st, k_gm_xupd, VGRID, RED_THREADS, 0, va, h->kz, h->kx);
   } else {
-    k_gm_xupd<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kp, h->kx);
+    launch_k(h->st, k_gm_xupd, VGRID, RED_THREADS, 0, va, h->kp, h->kx);
   }
   h->launches++;
   op_matvec(h, h->kx, h->kq, gU);
   if (!left) {
-    k_gm_restart<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kb, h->kq, V, 0);
+    launch_k(h->st, k_gm_restart, VGRID, RED_THREADS, 0, va, h->kb, h->kq, V, 0);
   } else {
     const long long ne = (long long)vs;
-    k_sub<<<592, 256, 0, h->st>>>(h->kb, h->kq, h->kr, ne);
+    launch_k(h->st, k_sub, 592, 256, 0, h->kb, h->kq, h->kr, ne);
     op_tau(h, h->kr, h->kz, gU);
-    k_gm_restart<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kb, h->kz, V, 1);
+    launch_k(h->st, k_gm_restart, VGRID, RED_THREADS, 0, va, h->kb, h->kz, V, 1);
     h->launches++;
   }
   h->launches++;
@@ -1282,13 +1307,13 @@ fde_status run_gmres(fde_handle h, const double* b, double* x, double rtol, int 
   const double* bd = stage_in(h, b, h->hin, bh);
   FDE_CUDA(cudaMemcpyAsync(h->kb, bd, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
   const VecArgs va = vec_args(h, rtol, maxit, restart, left);
-  k_reset_counters<<<1, 32, 0, h->st>>>(h->ctr, h->sst, h->batch);
+  launch_k(h->st, k_reset_counters, 1, 32, 0, h->ctr, h->sst, h->batch);
   h->launches++;
   if (!left) {
-    k_gm_init<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kb, h->kx, h->V);
+    launch_k(h->st, k_gm_init, VGRID, RED_THREADS, 0, va, h->kb, h->kx, h->V);
   } else {
     op_tau(h, h->kb, h->kz, nullptr);
-    k_gm_init<<<VGRID, RED_THREADS, 0, h->st>>>(va, h->kz, h->kx, h->V);
+    launch_k(h->st, k_gm_init, VGRID, RED_THREADS, 0, va, h->kz, h->kx, h->V);
   }
   h->launches++;
   FDE_CUDA(cudaGetLastError());
@@ -1477,7 +1502,7 @@ fde_status fde_profile_solve(fde_handle h, const double* b, double* x, double rt
     if (rs != FDE_OK && rs != FDE_ERR_NOT_CONVERGED) return rs;
     // 2. re-activate every RHS and run one more loop body (PCG iteration / GMRES
     //    cycle) kernel by kernel, each bracketed by CUDA events, no flush
-    k_reactivate<<<1, 32, 0, h->st>>>(h->ctr, h->sst, h->batch);
+    launch_k(h->st, k_reactivate, 1, 32, 0, h->ctr, h->sst, h->batch);
     FDE_CUDA(cudaGetLastError());
     h->flush = nullptr;
     h->flush_bytes = 0;

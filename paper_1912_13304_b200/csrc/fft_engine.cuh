@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "pdl.cuh"
+
 namespace fde {
 
 // Phase probes for tools/phase_probe.cu (compiled out unless FDE_PROBES is defined):

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "pdl.cuh"
+
 namespace fde {
 
 constexpr int RED_BLOCKS = 592;   // 4 x 148 SMs: enough loads in flight for HBM/L2 rate
@@ -131,6 +133,7 @@ __device__ __forceinline__ void mark_finished(VecArgs& a, SolveState& s) {
 // ============================================================ PCG (a3) ====
 // init: x = 0, r = b; ‖b‖
 __global__ void k_pcg_init(VecArgs a, const double* __restrict__ b, double* __restrict__ x, double* __restrict__ r) {
+  FDE_PDL_ENTRY();
   const int rb = blockIdx.y, N = a.N;
   const size_t o = (size_t)rb * N;
   double acc[1] = {0.0};
@@ -167,6 +170,7 @@ __global__ void k_pcg_init(VecArgs a, const double* __restrict__ b, double* __re
 
 // rho = r·z; p = 0 and β = 0, so that the first fused iteration's p = z + β p = z
 __global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const double* __restrict__ z, double* __restrict__ p) {
+  FDE_PDL_ENTRY();
   const int rb = blockIdx.y, N = a.N;
   const size_t o = (size_t)rb * N;
   double acc[1] = {0.0};
@@ -195,6 +199,7 @@ __global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const doubl
 
 // α = ρ / (p·q)
 __global__ void k_pcg_pq(VecArgs a, const double* __restrict__ p, const double* __restrict__ q) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -224,6 +229,7 @@ __global__ void k_pcg_pq(VecArgs a, const double* __restrict__ p, const double* 
 // x += α p ; r -= α q ; ‖r‖ ; convergence (‖r‖ <= rtol ‖b‖, R10)
 __global__ void k_pcg_xr(VecArgs a, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
                          double* __restrict__ r) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -263,6 +269,7 @@ __global__ void k_pcg_xr(VecArgs a, const double* __restrict__ p, const double* 
 
 // ρ' = r·z ; β = ρ'/ρ ; p = z + β p is done by k_pcg_p
 __global__ void k_pcg_rz(VecArgs a, const double* __restrict__ r, const double* __restrict__ z) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -291,6 +298,7 @@ __global__ void k_pcg_rz(VecArgs a, const double* __restrict__ r, const double* 
 }
 
 __global__ void k_pcg_p(VecArgs a, const double* __restrict__ z, double* __restrict__ p) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -303,6 +311,7 @@ __global__ void k_pcg_p(VecArgs a, const double* __restrict__ z, double* __restr
 // init: x = 0, r = b (right) ; ref = ‖r‖ ; V0 = r/‖r‖ (done by k_gm_scale)
 // For left preconditioning the caller passes r = P⁻¹b as `src`.
 __global__ void k_gm_init(VecArgs a, const double* __restrict__ src, double* x, double* V0) {
+  FDE_PDL_ENTRY();
   const int rb = blockIdx.y, N = a.N;
   const size_t o = (size_t)rb * N;
   double acc[1] = {0.0};
@@ -344,6 +353,7 @@ __global__ void k_gm_init(VecArgs a, const double* __restrict__ src, double* x, 
 
 // V_j *= inv_h (normalise the new basis vector in place)
 __global__ void k_gm_scale(VecArgs a, double* Vj) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -370,6 +380,7 @@ constexpr int MD_CH = 8;
 
 // CGS pass 1: h_i = V_iᵀ w, i = 0..j
 __global__ void k_gm_mdot(VecArgs a, const double* __restrict__ V, size_t vstride, const double* __restrict__ w, int j) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -389,6 +400,7 @@ __global__ void k_gm_mdot(VecArgs a, const double* __restrict__ V, size_t vstrid
 
 // CGS pass 1 update + pass 2 dots: w -= V h ; h2_i = V_iᵀ w
 __global__ void k_gm_upd_mdot(VecArgs a, const double* __restrict__ V, size_t vstride, double* w, int j) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -419,6 +431,7 @@ __global__ void k_gm_upd_mdot(VecArgs a, const double* __restrict__ V, size_t vs
 // registers (the vectors are read from HBM once instead of twice)
 __global__ void __launch_bounds__(RED_THREADS) k_gm_upd_mdot32(VecArgs a, const double* __restrict__ V, size_t vstride,
                                                                double* __restrict__ w, int j) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -460,6 +473,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_gm_upd_mdot32(VecArgs a, const 
 
 // CGS pass 2 update + norm + Arnoldi/Givens step (thread 0 of the last block)
 __global__ void k_gm_upd_norm(VecArgs a, const double* __restrict__ V, size_t vstride, double* w, int j) {
+  FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
@@ -526,6 +540,7 @@ __global__ void k_gm_upd_norm(VecArgs a, const double* __restrict__ V, size_t vs
 
 // end of cycle, step 1: y = R⁻¹ g (redundantly per block), u = Σ y_i V_i
 __global__ void k_gm_lincomb(VecArgs a, const double* __restrict__ V, size_t vstride, double* u) {
+  FDE_PDL_ENTRY();
   if (a.ctr->unfinished == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (a.st[rb].finished) return;
@@ -551,6 +566,7 @@ __global__ void k_gm_lincomb(VecArgs a, const double* __restrict__ V, size_t vst
 
 // end of cycle, step 2: x += z
 __global__ void k_gm_xupd(VecArgs a, const double* __restrict__ z, double* x) {
+  FDE_PDL_ENTRY();
   if (a.ctr->unfinished == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (a.st[rb].finished) return;
@@ -563,6 +579,7 @@ __global__ void k_gm_xupd(VecArgs a, const double* __restrict__ z, double* x) {
 //   right: V0 = b - t ; left: V0 = res (already the preconditioned residual)
 __global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const double* __restrict__ t, double* V0,
                              int res_ready) {
+  FDE_PDL_ENTRY();
   if (a.ctr->unfinished == 0) return;
   const int rb = blockIdx.y, N = a.N;
   SolveState& s0 = a.st[rb];
@@ -752,6 +769,7 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
 
 // PREC_NONE τ step of the fused PCG: x += α p, r -= α q, z = r (‖r‖² and r·z partials)
 __global__ void k_pcg_xrz_none(KryFuse k, int N, double* __restrict__ z) {
+  FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
   if (!k.st[rhs].cyc_active) return;
   const double al = k.st[rhs].alpha;
@@ -771,6 +789,7 @@ __global__ void k_pcg_xrz_none(KryFuse k, int N, double* __restrict__ z) {
 // while-loop control of a CUDA graph (conditional WHILE node): keep looping
 // while some RHS is still iterating, at most maxloops bodies.
 __global__ void k_loop_ctrl(cudaGraphConditionalHandle hdl, Counters* c, int maxloops) {
+  FDE_PDL_ENTRY();
   const int loops = c->loops + 1;
   c->loops = loops;
   cudaGraphSetConditional(hdl, (c->active > 0 && loops < maxloops) ? 1u : 0u);
@@ -778,14 +797,17 @@ __global__ void k_loop_ctrl(cudaGraphConditionalHandle hdl, Counters* c, int max
 
 // plain helpers -------------------------------------------------------------
 __global__ void k_copy(const double* __restrict__ src, double* dst, long long n) {
+  FDE_PDL_ENTRY();
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     dst[e] = src[e];
 }
 __global__ void k_sub(const double* __restrict__ b, const double* __restrict__ t, double* r, long long n) {
+  FDE_PDL_ENTRY();
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     r[e] = b[e] - t[e];
 }
 __global__ void k_scale_field(const double* __restrict__ src, const double* __restrict__ f, double* dst, int N, long long n) {
+  FDE_PDL_ENTRY();
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     dst[e] = src[e] * f[e % N];
 }

@@ -113,6 +113,7 @@ struct LineMap {
 template <int K, int k, bool COL, bool VAR, int FPC>
 __global__ void __launch_bounds__(FPC * (1 << (K - k)), min_blocks_for(FPC * (1 << (K - k))))
 k_toeplitz_lines(LineArgs a) {
+  FDE_PDL_ENTRY();
   using G = FftGeom<K, k>;
   using M = LineMap<G, COL, FPC>;
   extern __shared__ double2 smem_all[];

@@ -33,6 +33,7 @@ __device__ __forceinline__ double symbol_at(const LineArgs& a, int l, int e) {
 template <int KM, bool COL, int FPC, int MODE>
 __global__ void __launch_bounds__(FPC * (1 << (KM - 3)), min_blocks_for(FPC * (1 << (KM - 3))))
 k_sineop_lines(LineArgs a) {
+  FDE_PDL_ENTRY();
   using GD = FftGeom<KM, 3>;      // DST: length-m FFT, 8 points per thread
   using GT = FftGeom<KM + 1, 4>;  // Toeplitz: length-2m FFT, 16 points per thread
   static_assert(GD::P == GT::P, "one thread layout for both transforms");
@@ -206,6 +207,7 @@ k_sineop_lines(LineArgs a) {
 // r̂·ẑ = Σ r̂²/F (the diagonal preconditioner), finalised like KM_XR | KM_RZ.
 __global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, const double* __restrict__ Fx,
                                                  const double* __restrict__ Fy) {
+  FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
   if (!k.st[rhs].cyc_active) return;
   const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * n : (size_t)n);
@@ -228,6 +230,7 @@ __global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, con
 // sine-domain PCG start: x̂ = 0, p̂ = 0, ‖b̂‖, ρ = Σ r̂²/F, β = 0 (r̂ = b̂ already formed)
 __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, const double* __restrict__ Fx,
                                                    const double* __restrict__ Fy) {
+  FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
   const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * n : (size_t)n);
   double acc[3] = {0.0, 0.0, 0.0};
