@@ -219,7 +219,7 @@ template <int KM, bool COL, int MODE>
 struct LaunchCfgS {
   using GT = FftGeom<KM + 1, 4>;
   static constexpr int P = 1 << (KM - 3);
-  static constexpr int SPG = GT::SM_STRIDE * 16 + (MODE == 1 ? FftGeom<KM, 3>::SM_STRIDE * 16 : 0);
+  static constexpr int SPG = GT::SM_STRIDE * 16 + ((MODE == 1 || MODE == 4) ? FftGeom<KM, 3>::SM_STRIDE * 16 : 0);
   static constexpr int BY_SMEM = (200 * 1024) / SPG > 0 ? (200 * 1024) / SPG : 1;
   static constexpr int BY_THR = 512 / P > 0 ? 512 / P : 1;
 #ifndef FDE_SINE_COL_FPC
@@ -229,7 +229,8 @@ struct LaunchCfgS {
   static constexpr int FPC0 = WANT < BY_THR ? WANT : BY_THR;
   static constexpr int FPC = FPC0 < BY_SMEM ? FPC0 : BY_SMEM;
   static constexpr int THREADS = FPC * P;
-  static constexpr int SCR = (FPC * (GroupScan<COL, P, FPC>::NSEG + 1) * 2) * 8;
+  static constexpr int SCR0 = (FPC * (GroupScan<COL, P, FPC>::NSEG + 1) * 2) * 8;
+  static constexpr int SCR = SCR0 > 96 * 8 ? SCR0 : 96 * 8;   // also block_reduce3's scratch
   static constexpr int SMEM = FPC * SPG + SCR;
 };
 
@@ -282,6 +283,7 @@ struct fde_handle_s {
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
   bool no_graph = false;            // env FDE_GRAPH=0: host-driven loop (for profilers)
+  bool sine_legacy = true;          // 3-kernel sine-domain body; env FDE_SINE_BODY=2: the recurrence body (A/B)
   std::vector<void*> allocs;
   // profiling (fde_profile_unit)
   bool prof = false;
@@ -378,7 +380,7 @@ void launch_sineop_k(fde_handle h, const LineArgs& a) {
   }
   const int npairs = (a.nlines + 1) / 2;
   const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
-  launch_named(h, MODE == 0 ? "sine_op_rows" : (MODE == 1 ? "sine_op_cols" : "sine_op_1d"),
+  launch_named(h, (MODE == 0 || MODE == 3) ? "sine_op_rows" : ((MODE == 1 || MODE == 4) ? "sine_op_cols" : "sine_op_1d"),
                [&] { launch_k(h->st, kern, grid, C::THREADS, C::SMEM, a); });
 }
 
@@ -880,6 +882,8 @@ void build(fde_handle h, const fde_desc* d) {
     h->force_standard_pcg = e && std::strcmp(e, "standard") == 0;
     const char* g = std::getenv("FDE_GRAPH");
     h->no_graph = g && std::strcmp(g, "0") == 0;
+    const char* sb = std::getenv("FDE_SINE_BODY");
+    h->sine_legacy = !(sb && std::strcmp(sb, "2") == 0);
     const char* pd = std::getenv("FDE_PDL");
     g_pdl = pd && std::strcmp(pd, "1") == 0;
   }
@@ -1147,6 +1151,36 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
   a.Fx = h->Fx;
   a.Fy = h->dims == 2 ? h->Fy : nullptr;
   a.mu = h->mus_x;
+  if (!h->sine_legacy) {
+    // body k: 2D = rows (r, x update, ẑ = r/F, convergence, β) + columns (q = Aẑ + βq,
+    // p = ẑ + βp, α); 1D = one kernel with CTA-local reductions
+    if (h->dims == 2) {
+      a.nlines = h->n;
+      a.y = h->wx;
+      a.kf = kf;
+      a.kf.mode = KM_SROW | KM_GATE;
+      FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 3>(h, a)));
+      LineArgs b = base_args(h);
+      b.Fx = h->Fx;
+      b.Fy = h->Fy;
+      b.nlines = h->n;
+      b.yin = h->wx;
+      b.y = h->kq;
+      b.mu = h->mus_y;
+      b.nu = h->d.nu;
+      b.kf = kf;
+      b.kf.mode = KM_PQ | KM_GATE;
+      FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, true, 4>(h, b)));
+    } else {
+      a.nlines = 1;
+      a.y = h->kq;
+      a.nu = h->d.nu;
+      a.kf = kf;
+      a.kf.mode = KM_GATE;
+      FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 5>(h, a)));
+    }
+    return;
+  }
   if (h->dims == 2) {
     a.nlines = h->n;
     a.x = h->kr;

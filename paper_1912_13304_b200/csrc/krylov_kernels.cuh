@@ -35,7 +35,7 @@ struct SolveState {          // one per RHS, device resident
   int status;                // ST_*
   int kused;                 // GMRES: steps taken in the current cycle
   int restarts;
-  int pad;
+  int kbody;                 // sine-domain PCG: loop bodies started (body k forms r_k)
 };
 
 struct GmresSmall {          // one per RHS
@@ -636,9 +636,11 @@ __global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const doub
 //            partial ‖r‖² -> iteration count and convergence (R10)
 //   KM_RZ    epilogue of the last τ kernel:   partial r·z -> ρ' , β = ρ'/ρ
 //   KM_GATE  no vector work; CTAs of finished RHS exit
+//   KM_SROW  sine-domain body k (sine_kernels.cuh MODE 3): ‖r_k‖² -> iterations
+//            (= k) and convergence for k >= 1; ρ_k = r_k·z_k -> β_k = ρ_k/ρ_{k-1}
 // Partials: kpart[(rhs*3 + slot)*KPMAX + blockIdx.x]; the last CTA of each RHS
 // (ticket) sums them in fixed order (deterministic) and updates SolveState.
-enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16, KM_INIT = 32 };
+enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16, KM_INIT = 32, KM_SROW = 64 };
 constexpr int KPMAX = 4096;   // CTAs per RHS of one line kernel
 
 struct KryFuse {
@@ -646,7 +648,7 @@ struct KryFuse {
   double* p;
   double* x;
   double* r;
-  const double* q;
+  double* q;
   SolveState* st;
   Counters* ctr;
   double* part;
@@ -716,6 +718,8 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
     s.bnorm = sqrt(tot[1]);
     s.rho = tot[2];
     s.betac = 0.0;
+    s.alpha = 0.0;
+    s.kbody = 0;
     s.iters = 0;
     s.converged = 0;
     s.status = ST_OK;
@@ -731,6 +735,34 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
       finish_rhs(k.ctr, s);
     }
     return;
+  }
+  if (k.mode & KM_SROW) {
+    const int kb = s.kbody;
+    s.kbody = kb + 1;
+    if (kb >= 1) {
+      const double rn = sqrt(tot[1]);
+      s.iters = kb;
+      s.rnorm = rn / s.bnorm;
+      if (!isfinite(rn)) {
+        s.status = ST_NONFINITE;
+        finish_rhs(k.ctr, s);
+      } else if (rn <= k.rtol * s.bnorm) {
+        s.converged = 1;
+        finish_rhs(k.ctr, s);
+      } else if (kb >= k.maxit) {
+        finish_rhs(k.ctr, s);
+      }
+    }
+    if (s.cyc_active) {
+      const double rz = tot[2];
+      if (!(rz > 0.0)) {
+        s.status = isfinite(rz) ? ST_NOT_SPD : ST_NONFINITE;
+        finish_rhs(k.ctr, s);
+      } else {
+        s.betac = kb >= 1 ? rz / s.rho : 0.0;
+        s.rho = rz;
+      }
+    }
   }
   if (k.mode & KM_PQ) {
     const double pq = tot[0];

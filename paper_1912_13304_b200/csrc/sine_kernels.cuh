@@ -18,6 +18,28 @@
 
 namespace fde {
 
+// CTA-wide fixed-order sum of acc[0..2]; the result is valid in thread 0.
+// scr: >= 3*32 doubles of shared memory; ends with a barrier.
+__device__ __forceinline__ void block_reduce3(double (&acc)[3], double* scr) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double v = warp_sum(acc[i]);
+    if (lane == 0) scr[i * 32 + wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += scr[i * 32 + w];
+      acc[i] = s;
+    }
+  }
+  __syncthreads();
+}
+
 // symbol F at element e of line l (2D rows: x index e, y index l; 2D cols:
 // x index l, y index e; 1D: Fy == nullptr)
 template <bool COL>
@@ -26,6 +48,18 @@ __device__ __forceinline__ double symbol_at(const LineArgs& a, int l, int e) {
   return COL ? a.Fx[l] + a.Fy[e] : a.Fx[e] + a.Fy[l];
 }
 
+// Two loop bodies are implemented. The recurrence body (MODES 3-5,
+// FDE_SINE_BODY=2) uses the standard recurrence q = A z + β q (p = z + β p):
+// MODE 3: 2D rows, body k: r̂ -= α q̂, x̂ += α p̂ (α_{k-1}; written back),
+//         ẑ = r̂/F, partials ‖r̂‖², r̂·ẑ (KM_SROW: convergence, β_k), y = (S T̃_α S) ẑ
+// MODE 4: 2D columns: w = ν ẑ + yin + (S T̃_β S) ẑ, q̂ = w + β q̂, p̂ = ẑ + β p̂
+//         (written back), partial p̂·q̂ (KM_PQ: α_k)
+// MODE 5: 1D, one CTA per RHS: MODE 3 + MODE 4 in one kernel, both
+//         reductions inside the CTA (no grid-wide step at all)
+// so a 2D iteration is 2 kernels and a 1D one is 1 — but measured slower on
+// the B200 (cfg 5 n=1023: 148 vs 90 µs/iteration): the column pass then does
+// the vector recurrences in the strided column layout. The default body
+// (MODES 0-2 + k_sine_xr, 3 kernels) applies the operator to p̂:
 // MODE 0: 2D row pass:   p̂ = r̂/F + β p̂ (written back), y = (S T̃_α S) p̂ along rows
 // MODE 1: 2D column pass: y = q̂ = ν p̂ + yin + (S T̃_β S) p̂ along columns, partial p̂·q̂
 // MODE 2: 1D:            p̂ = r̂/F + β p̂, y = q̂ = ν p̂ + (S T̃ S) p̂, partial p̂·q̂
@@ -44,7 +78,7 @@ k_sineop_lines(LineArgs a) {
   const int f = M::group(), t = M::lane();
   double2* sm = smem_all + (size_t)f * GT::SM_STRIDE;
   double2* smW = smem_all + (size_t)FPC * GT::SM_STRIDE + (size_t)f * GD::SM_STRIDE;
-  double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * (GT::SM_STRIDE + (MODE == 1 ? GD::SM_STRIDE : 0)));
+  double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * (GT::SM_STRIDE + ((MODE == 1 || MODE == 4) ? GD::SM_STRIDE : 0)));
   const TwSrc twd{nullptr, a.twpm}, twt{nullptr, a.twp};
   const int g = blockIdx.x * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
@@ -52,17 +86,40 @@ k_sineop_lines(LineArgs a) {
   const int n = m - 1;
   const Line A0 = line_of<COL>(v0 ? l0 : 0, blockIdx.y, n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, blockIdx.y, n, a.N);
 
-  // 1. stage p̂ in shared memory (natural order, position e+1)
-  const double beta = MODE != 1 ? a.kf.st[blockIdx.y].betac : 0.0;
+  // 1. stage the operator input in shared memory (natural order)
+  SolveState* const sst = a.kf.st + blockIdx.y;
+  const double beta = (MODE == 0 || MODE == 2) ? sst->betac : 0.0;
+  const double alpha = (MODE == 3 || MODE == 5) ? sst->alpha : 0.0;
+  double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int i = 0; i < RD; ++i) {
     const int e = t + P * i;
     if (e < n) {
       const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
       double p0 = 0.0, p1 = 0.0;
-      if (MODE != 1) {  // p̂ = ẑ + β p̂ with ẑ = r̂ / F (the τ-solve is diagonal here)
+      if (MODE == 0 || MODE == 2) {  // p̂ = ẑ + β p̂ with ẑ = r̂ / F (the τ-solve is diagonal here)
         if (v0) { p0 = fma(beta, a.kf.p[o0], __ldg(a.x + o0) * fast_rcp(symbol_at<COL>(a, l0, e))); a.kf.p[o0] = p0; }
         if (v1) { p1 = fma(beta, a.kf.p[o1], __ldg(a.x + o1) * fast_rcp(symbol_at<COL>(a, l1, e))); a.kf.p[o1] = p1; }
+      } else if (MODE == 3 || MODE == 5) {  // r̂ -= α q̂, x̂ += α p̂, ẑ = r̂/F
+        if (v0) {
+          const double r = fma(-alpha, a.kf.q[o0], a.kf.r[o0]);
+          a.kf.r[o0] = r;
+          a.kf.x[o0] = fma(alpha, a.kf.p[o0], a.kf.x[o0]);
+          p0 = r * fast_rcp(symbol_at<COL>(a, l0, e));
+          acc[1] = fma(r, r, acc[1]);
+          acc[2] = fma(r, p0, acc[2]);
+        }
+        if (v1) {
+          const double r = fma(-alpha, a.kf.q[o1], a.kf.r[o1]);
+          a.kf.r[o1] = r;
+          a.kf.x[o1] = fma(alpha, a.kf.p[o1], a.kf.x[o1]);
+          p1 = r * fast_rcp(symbol_at<COL>(a, l1, e));
+          acc[1] = fma(r, r, acc[1]);
+          acc[2] = fma(r, p1, acc[2]);
+        }
+      } else if (MODE == 4) {  // ẑ = r̂/F
+        if (v0) p0 = a.kf.r[o0] * fast_rcp(symbol_at<COL>(a, l0, e));
+        if (v1) p1 = a.kf.r[o1] * fast_rcp(symbol_at<COL>(a, l1, e));
       } else {
         if (v0) p0 = __ldg(a.x + o0);
         if (v1) p1 = __ldg(a.x + o1);
@@ -70,7 +127,35 @@ k_sineop_lines(LineArgs a) {
       sm[GD::swz(e)] = make_double2(p0, p1);
     }
   }
-  if (MODE == 1 && a.yin) {  // the row pass's result streams in for the epilogue (chunk layout)
+  double beta5 = 0.0;
+  if (MODE == 5) {  // 1D: the whole line is in this CTA -> β_k here, no grid step
+    block_reduce3(acc, scr);
+    __shared__ int s_go;
+    if (threadIdx.x == 0) {
+      SolveState& s = *sst;
+      const int kb = s.kbody;
+      s.kbody = kb + 1;
+      if (kb >= 1) {
+        const double rn = sqrt(acc[1]);
+        s.iters = kb;
+        s.rnorm = rn / s.bnorm;
+        if (!isfinite(rn)) { s.status = ST_NONFINITE; finish_rhs(a.kf.ctr, s); }
+        else if (rn <= a.kf.rtol * s.bnorm) { s.converged = 1; finish_rhs(a.kf.ctr, s); }
+        else if (kb >= a.kf.maxit) finish_rhs(a.kf.ctr, s);
+      }
+      if (s.cyc_active) {
+        if (!(acc[2] > 0.0)) { s.status = isfinite(acc[2]) ? ST_NOT_SPD : ST_NONFINITE; finish_rhs(a.kf.ctr, s); }
+        else { s.betac = kb >= 1 ? acc[2] / s.rho : 0.0; s.rho = acc[2]; }
+      }
+      s_go = s.cyc_active;
+      scr[0] = s.betac;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    beta5 = scr[0];
+    __syncthreads();
+  }
+  if ((MODE == 1 || MODE == 4) && a.yin) {  // the row pass's result streams in for the epilogue (chunk layout)
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
       const int e = RD * t + i - 1;
@@ -126,8 +211,34 @@ k_sineop_lines(LineArgs a) {
   dstm_post<GD, COL, FPC>(vd, sm, scr, t, f, g0, g1);
 
   // 6. epilogue
-  double acc[3] = {0.0, 0.0, 0.0};
-  if (MODE == 1) {
+  if (MODE == 4) {
+    // columns, recurrence body: w = ν ẑ + yin + op, q̂ = w + β q̂, p̂ = ẑ + β p̂
+    if (a.yin) cp_async_wait_all();
+    const double b4 = sst->betac;
+#pragma unroll
+    for (int i = 0; i < RD; ++i) {
+      const int e = RD * t + i - 1;
+      if (e < 0) continue;
+      if (v0) {
+        const long long o = A0.base + (long long)e * A0.stride;
+        const double z = a.kf.r[o] * fast_rcp(symbol_at<COL>(a, l0, e));
+        const double w = fma(a.nu, z, g0[i] + (a.yin ? smW[GD::swz(e)].x : 0.0));
+        const double qv = fma(b4, a.y[o], w), pv = fma(b4, a.kf.p[o], z);
+        a.y[o] = qv;
+        a.kf.p[o] = pv;
+        acc[0] = fma(pv, qv, acc[0]);
+      }
+      if (v1) {
+        const long long o = A1.base + (long long)e * A1.stride;
+        const double z = a.kf.r[o] * fast_rcp(symbol_at<COL>(a, l1, e));
+        const double w = fma(a.nu, z, g1[i] + (a.yin ? smW[GD::swz(e)].y : 0.0));
+        const double qv = fma(b4, a.y[o], w), pv = fma(b4, a.kf.p[o], z);
+        a.y[o] = qv;
+        a.kf.p[o] = pv;
+        acc[0] = fma(pv, qv, acc[0]);
+      }
+    }
+  } else if (MODE == 1) {
     // columns: this lane owns rows e = RD t + i - 1 of its two columns
     if (a.yin) cp_async_wait_all();
 #pragma unroll
@@ -162,9 +273,24 @@ k_sineop_lines(LineArgs a) {
       if (e >= n) continue;
       const double2 o = sm[GD::swz(e)];
       const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
-      if (MODE == 0) {
+      if (MODE == 0 || MODE == 3) {
         if (v0) a.y[o0] = o.x;
         if (v1) a.y[o1] = o.y;
+      } else if (MODE == 5) {  // 1D recurrence body: q̂ = ν ẑ + (S T̃ S) ẑ + β q̂, p̂ = ẑ + β p̂
+        if (v0) {
+          const double z = a.kf.r[o0] * fast_rcp(symbol_at<COL>(a, l0, e));
+          const double qv = fma(beta5, a.y[o0], fma(a.nu, z, o.x)), pv = fma(beta5, a.kf.p[o0], z);
+          a.y[o0] = qv;
+          a.kf.p[o0] = pv;
+          acc[0] = fma(pv, qv, acc[0]);
+        }
+        if (v1) {
+          const double z = a.kf.r[o1] * fast_rcp(symbol_at<COL>(a, l1, e));
+          const double qv = fma(beta5, a.y[o1], fma(a.nu, z, o.y)), pv = fma(beta5, a.kf.p[o1], z);
+          a.y[o1] = qv;
+          a.kf.p[o1] = pv;
+          acc[0] = fma(pv, qv, acc[0]);
+        }
       } else {  // 1D: q̂ = ν p̂ + (S T̃ S) p̂, p̂·q̂
         if (v0) {
           const double pv = a.kf.p[o0], qv = fma(a.nu, pv, o.x);
@@ -179,7 +305,19 @@ k_sineop_lines(LineArgs a) {
       }
     }
   }
-  if (MODE != 0) kry_reduce_finalize(a.kf, acc);
+  if (MODE == 5) {  // α_k = ρ_k / (p̂·q̂) inside the CTA
+    acc[1] = acc[2] = 0.0;
+    block_reduce3(acc, scr);
+    if (threadIdx.x == 0) {
+      SolveState& s = *sst;
+      if (!(acc[0] > 0.0)) { s.status = isfinite(acc[0]) ? ST_NOT_SPD : ST_NONFINITE; finish_rhs(a.kf.ctr, s); }
+      else s.alpha = s.rho / acc[0];
+    }
+  } else if (MODE == 1 || MODE == 2 || MODE == 4) {
+    kry_reduce_finalize(a.kf, acc);
+  } else if (MODE == 3) {
+    kry_reduce_finalize(a.kf, acc);
+  }
 }
 
 // F at (i, j) in the sine domain (1D: Fy == nullptr)
@@ -238,6 +376,7 @@ __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, c
     const double rv = k.r[o + e];
     k.x[o + e] = 0.0;
     k.p[o + e] = 0.0;
+    k.q[o + e] = 0.0;
     acc[1] = fma(rv, rv, acc[1]);
     acc[2] = fma(rv * rv, fast_rcp(F), acc[2]);
   })
