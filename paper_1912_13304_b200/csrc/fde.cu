@@ -1212,7 +1212,11 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
   const double* Fx = h->Fx;
   const double* Fy = h->dims == 2 ? h->Fy : nullptr;
   const int n = h->n, dims = h->dims;
-  const int gx = dims == 2 ? std::min(n, KPMAX) : 64;
+  static const int xr_grid = [] {
+    const char* e = std::getenv("FDE_XR_GRID");
+    return e ? std::atoi(e) : 592;
+  }();
+  const int gx = dims == 2 ? std::min(n, xr_grid) : 64;
   launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr, dim3(gx, h->batch), 256, 0, kv, n, dims, Fx, Fy); });
 }
 

@@ -91,38 +91,63 @@ k_sineop_lines(LineArgs a) {
   const double beta = (MODE == 0 || MODE == 2) ? sst->betac : 0.0;
   const double alpha = (MODE == 3 || MODE == 5) ? sst->alpha : 0.0;
   double acc[3] = {0.0, 0.0, 0.0};
+  {
+    // phase 1: every global load of this thread's RD elements (no stores in
+    // between, so they are all in flight together); phase 2: arithmetic,
+    // write-backs and the shared-memory staging
+    constexpr int NV = (MODE == 3 || MODE == 5) ? 4 : ((MODE == 0 || MODE == 2) ? 2 : 1);
+    double g0v[NV][RD], g1v[NV][RD], f0v[RD], f1v[RD];
 #pragma unroll
-  for (int i = 0; i < RD; ++i) {
-    const int e = t + P * i;
-    if (e < n) {
+    for (int i = 0; i < RD; ++i) {
+      const int e = t + P * i;
+      const bool ok = e < n;
+      const long long o0 = A0.base + (long long)(ok ? e : 0) * A0.stride, o1 = A1.base + (long long)(ok ? e : 0) * A1.stride;
+      const double* src[4];
+      if (MODE == 3 || MODE == 5) { src[0] = a.kf.r; src[1] = a.kf.q; src[2] = a.kf.p; src[3] = a.kf.x; }
+      else if (MODE == 0 || MODE == 2) { src[0] = a.x; src[1] = a.kf.p; }
+      else if (MODE == 4) { src[0] = a.kf.r; }
+      else { src[0] = a.x; }
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        g0v[c][i] = (ok && v0) ? src[c][o0] : 0.0;
+        g1v[c][i] = (ok && v1) ? src[c][o1] : 0.0;
+      }
+      if (MODE != 1) {
+        f0v[i] = (ok && v0) ? symbol_at<COL>(a, l0, e) : 1.0;
+        f1v[i] = (ok && v1) ? symbol_at<COL>(a, l1, e) : 1.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RD; ++i) {
+      const int e = t + P * i;
+      if (e >= n) continue;
       const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
       double p0 = 0.0, p1 = 0.0;
       if (MODE == 0 || MODE == 2) {  // p̂ = ẑ + β p̂ with ẑ = r̂ / F (the τ-solve is diagonal here)
-        if (v0) { p0 = fma(beta, a.kf.p[o0], __ldg(a.x + o0) * fast_rcp(symbol_at<COL>(a, l0, e))); a.kf.p[o0] = p0; }
-        if (v1) { p1 = fma(beta, a.kf.p[o1], __ldg(a.x + o1) * fast_rcp(symbol_at<COL>(a, l1, e))); a.kf.p[o1] = p1; }
+        p0 = fma(beta, g0v[1][i], g0v[0][i] * fast_rcp(f0v[i]));
+        p1 = fma(beta, g1v[1][i], g1v[0][i] * fast_rcp(f1v[i]));
+        if (v0) a.kf.p[o0] = p0;
+        if (v1) a.kf.p[o1] = p1;
       } else if (MODE == 3 || MODE == 5) {  // r̂ -= α q̂, x̂ += α p̂, ẑ = r̂/F
+        const double r0 = fma(-alpha, g0v[1][i], g0v[0][i]), r1 = fma(-alpha, g1v[1][i], g1v[0][i]);
+        p0 = r0 * fast_rcp(f0v[i]);
+        p1 = r1 * fast_rcp(f1v[i]);
         if (v0) {
-          const double r = fma(-alpha, a.kf.q[o0], a.kf.r[o0]);
-          a.kf.r[o0] = r;
-          a.kf.x[o0] = fma(alpha, a.kf.p[o0], a.kf.x[o0]);
-          p0 = r * fast_rcp(symbol_at<COL>(a, l0, e));
-          acc[1] = fma(r, r, acc[1]);
-          acc[2] = fma(r, p0, acc[2]);
+          a.kf.r[o0] = r0;
+          a.kf.x[o0] = fma(alpha, g0v[2][i], g0v[3][i]);
         }
         if (v1) {
-          const double r = fma(-alpha, a.kf.q[o1], a.kf.r[o1]);
-          a.kf.r[o1] = r;
-          a.kf.x[o1] = fma(alpha, a.kf.p[o1], a.kf.x[o1]);
-          p1 = r * fast_rcp(symbol_at<COL>(a, l1, e));
-          acc[1] = fma(r, r, acc[1]);
-          acc[2] = fma(r, p1, acc[2]);
+          a.kf.r[o1] = r1;
+          a.kf.x[o1] = fma(alpha, g1v[2][i], g1v[3][i]);
         }
+        acc[1] = fma(r0, r0, fma(r1, r1, acc[1]));
+        acc[2] = fma(r0, p0, fma(r1, p1, acc[2]));
       } else if (MODE == 4) {  // ẑ = r̂/F
-        if (v0) p0 = a.kf.r[o0] * fast_rcp(symbol_at<COL>(a, l0, e));
-        if (v1) p1 = a.kf.r[o1] * fast_rcp(symbol_at<COL>(a, l1, e));
+        p0 = g0v[0][i] * fast_rcp(f0v[i]);
+        p1 = g1v[0][i] * fast_rcp(f1v[i]);
       } else {
-        if (v0) p0 = __ldg(a.x + o0);
-        if (v1) p1 = __ldg(a.x + o1);
+        p0 = g0v[0][i];
+        p1 = g1v[0][i];
       }
       sm[GD::swz(e)] = make_double2(p0, p1);
     }
@@ -343,6 +368,9 @@ k_sineop_lines(LineArgs a) {
 
 // PCG vector step in the sine domain: x̂ += α p̂, r̂ -= α q̂, partials ‖r̂‖² and
 // r̂·ẑ = Σ r̂²/F (the diagonal preconditioner), finalised like KM_XR | KM_RZ.
+// 2D: a block per row (strided over rows); every thread issues the loads of
+// its XR_U elements of the row before any arithmetic (loads in flight).
+constexpr int XR_U = 4;
 __global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, const double* __restrict__ Fx,
                                                  const double* __restrict__ Fy) {
   FDE_PDL_ENTRY();
@@ -355,13 +383,35 @@ __global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, con
   const double* __restrict__ pr = k.p + o;
   const double* __restrict__ qr = k.q + o;
   double acc[3] = {0.0, 0.0, 0.0};
-  FDE_SINE_LOOP({
-    const double rv = fma(-al, qr[e], rr[e]);
-    rr[e] = rv;
-    xr[e] = fma(al, pr[e], xr[e]);
-    acc[1] = fma(rv, rv, acc[1]);
-    acc[2] = fma(rv * rv, fast_rcp(F), acc[2]);
-  })
+  const int rows = dims == 2 ? n : 1;
+  for (int j = blockIdx.x; j < rows; j += gridDim.x) {
+    const double fy = dims == 2 ? Fy[j] : 0.0;
+    const size_t rb = (size_t)j * n;
+    for (int i0 = threadIdx.x; i0 < n; i0 += XR_U * blockDim.x) {
+      double qv[XR_U], rv[XR_U], pv[XR_U], xv[XR_U], fv[XR_U];
+#pragma unroll
+      for (int u = 0; u < XR_U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        const bool ok = i < n;
+        qv[u] = ok ? qr[rb + i] : 0.0;
+        rv[u] = ok ? rr[rb + i] : 0.0;
+        pv[u] = ok ? pr[rb + i] : 0.0;
+        xv[u] = ok ? xr[rb + i] : 0.0;
+        fv[u] = ok ? Fx[i] + fy : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < XR_U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        const double r = fma(-al, qv[u], rv[u]);
+        if (i < n) {
+          rr[rb + i] = r;
+          xr[rb + i] = fma(al, pv[u], xv[u]);
+        }
+        acc[1] = fma(r, r, acc[1]);
+        acc[2] = fma(r * r, fast_rcp(fv[u]), acc[2]);
+      }
+    }
+  }
   kry_reduce_finalize(k, acc);
 }
 
