@@ -284,6 +284,7 @@ struct fde_handle_s {
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
   bool no_graph = false;            // env FDE_GRAPH=0: host-driven loop (for profilers)
   bool sine_legacy = true;          // 3-kernel sine-domain body; env FDE_SINE_BODY=2: the recurrence body (A/B)
+  bool sine1d_graph = false;        // env FDE_SINE1D=graph: 1D PCG per-iteration graph instead of one persistent kernel
   std::vector<void*> allocs;
   // profiling (fde_profile_unit)
   bool prof = false;
@@ -884,6 +885,8 @@ void build(fde_handle h, const fde_desc* d) {
     h->no_graph = g && std::strcmp(g, "0") == 0;
     const char* sb = std::getenv("FDE_SINE_BODY");
     h->sine_legacy = !(sb && std::strcmp(sb, "2") == 0);
+    const char* s1 = std::getenv("FDE_SINE1D");
+    h->sine1d_graph = s1 && std::strcmp(s1, "graph") == 0;
     const char* pd = std::getenv("FDE_PDL");
     g_pdl = pd && std::strcmp(pd, "1") == 0;
   }
@@ -1233,13 +1236,29 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   const int n = h->n, dims = h->dims;
   const int gx = dims == 2 ? std::min(n, KPMAX) : 64;
   launch_named(h, "sine_init", [&] { launch_k(h->st, k_sine_init, dim3(gx, h->batch), 256, 0, kf, n, dims, Fx, Fy); });
-  if (!h->no_graph && (!h->g_pcg || h->g_rtol != rtol || h->g_maxit != maxit)) {
+  const bool persist1d = h->dims == 1 && !h->sine1d_graph;
+  if (persist1d) {
+    // 1D: the whole solve in ONE kernel, one CTA per RHS (the line fits in a
+    // CTA, so both reductions of a body are CTA-local; recurrence body MODE 5)
+    LineArgs a = base_args(h);
+    a.Fx = h->Fx;
+    a.Fy = nullptr;
+    a.mu = h->mus_x;
+    a.nlines = 1;
+    a.y = h->kq;
+    a.nu = h->d.nu;
+    a.kf = kf;
+    a.kf.mode = KM_GATE;
+    a.persist = 1;
+    FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 5>(h, a)));
+  } else if (!h->no_graph && (!h->g_pcg || h->g_rtol != rtol || h->g_maxit != maxit)) {
     if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
     h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { sine_iteration(h, rtol, maxit); });
     h->g_rtol = rtol;
     h->g_maxit = maxit;
   }
-  if (h->no_graph) {  // FDE_GRAPH=0 (profilers): the same loop body from the host
+  if (persist1d) {
+  } else if (h->no_graph) {  // FDE_GRAPH=0 (profilers): the same loop body from the host
     for (int it = 0; it <= maxit; ++it) {
       sine_iteration(h, rtol, maxit);
       if ((it & 7) == 7 && read_active(h) == 0) break;
@@ -1253,7 +1272,7 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   op_dst_all(h, h->kx, xdev ? x : h->hout, h->dims == 2 ? s * s : s);
   if (!xdev) FDE_CUDA(cudaMemcpyAsync(x, h->hout, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   const fde_status ws = worst_status(h, st, true);
-  if (!h->no_graph) h->launches += (long long)read_loops(h) * h->g_pcg_nodes;
+  if (!h->no_graph && !persist1d) h->launches += (long long)read_loops(h) * h->g_pcg_nodes;
   return ws;
 }
 

@@ -46,6 +46,7 @@ struct LineArgs {
   double oscale;          // DST kernels: output scale (0 = 1)
   double2* zscr;          // variable Toeplitz: global scratch for the forward spectrum (L per line pair)
   int probe;              // phase-probe slot (FDE_PROBES builds only)
+  int persist;            // sine-domain 1D body (MODE 5): loop inside the kernel until the RHS finishes
   KryFuse kf;             // fused PCG vector work (krylov_kernels.cuh); kf.mode = 0: none
 };
 

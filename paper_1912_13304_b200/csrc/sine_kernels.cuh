@@ -86,6 +86,7 @@ k_sineop_lines(LineArgs a) {
   const int n = m - 1;
   const Line A0 = line_of<COL>(v0 ? l0 : 0, blockIdx.y, n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, blockIdx.y, n, a.N);
 
+  for (;;) {  // one loop body; MODE 5 with a.persist repeats it until the RHS finishes
   // 1. stage the operator input in shared memory (natural order)
   SolveState* const sst = a.kf.st + blockIdx.y;
   const double beta = (MODE == 0 || MODE == 2) ? sst->betac : 0.0;
@@ -342,6 +343,9 @@ k_sineop_lines(LineArgs a) {
     kry_reduce_finalize(a.kf, acc);
   } else if (MODE == 3) {
     kry_reduce_finalize(a.kf, acc);
+  }
+  if (MODE != 5 || !a.persist) break;
+  __syncthreads();  // persistent 1D solve: the next body reuses sm and reads this body's writes
   }
 }
 

@@ -154,7 +154,7 @@ def test_pcg_sine_domain_and_standard_paths_agree_with_oracle(torch_cuda, cfg, n
     p = W.config(cfg, n=n, batch=batch)
     s = oracle_system(p)
     ref = oracle_solve(p, s, "pcg")
-    for env in ({}, {"FDE_SINE_BODY": "2"}, {"FDE_PCG": "standard"}):
+    for env in ({}, {"FDE_SINE_BODY": "2"}, {"FDE_PCG": "standard"}, {"FDE_SINE1D": "graph"}):
         stats, x = _solve_with_env(torch_cuda, p, env)
         for b in range(batch):
             xo, it_o, conv_o, _ = ref[b]
