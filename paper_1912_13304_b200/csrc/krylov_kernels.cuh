@@ -197,116 +197,6 @@ __global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const doubl
   }
 }
 
-// α = ρ / (p·q)
-__global__ void k_pcg_pq(VecArgs a, const double* __restrict__ p, const double* __restrict__ q) {
-  FDE_PDL_ENTRY();
-  if (a.ctr->active == 0) return;
-  const int rb = blockIdx.y, N = a.N;
-  if (!a.st[rb].cyc_active) return;
-  const size_t o = (size_t)rb * N;
-  double acc[1] = {0.0};
-  FDE_GRID_LOOP(e) acc[0] = fma(p[o + e], q[o + e], acc[0]);
-  __shared__ double red[32];
-  block_sum<1>(acc, red);
-  double* part = a.part + (size_t)rb * RED_BLOCKS;
-  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
-  if (last_block(&a.ctr->tickets[rb * 8])) {
-    __shared__ double out[1];
-    finalize(part, 1, out);
-    if (threadIdx.x == 0) {
-      SolveState& s = a.st[rb];
-      const double pq = out[0];
-      if (!(pq > 0.0)) {
-        s.status = isfinite(pq) ? ST_NOT_SPD : ST_NONFINITE;
-        mark_finished(a, s);
-      } else {
-        s.alpha = s.rho / pq;
-      }
-    }
-  }
-}
-
-// x += α p ; r -= α q ; ‖r‖ ; convergence (‖r‖ <= rtol ‖b‖, R10)
-__global__ void k_pcg_xr(VecArgs a, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
-                         double* __restrict__ r) {
-  FDE_PDL_ENTRY();
-  if (a.ctr->active == 0) return;
-  const int rb = blockIdx.y, N = a.N;
-  if (!a.st[rb].cyc_active) return;
-  const double al = a.st[rb].alpha;
-  const size_t o = (size_t)rb * N;
-  double acc[1] = {0.0};
-  FDE_GRID_LOOP(e) {
-    x[o + e] = fma(al, p[o + e], x[o + e]);
-    const double rv = fma(-al, q[o + e], r[o + e]);
-    r[o + e] = rv;
-    acc[0] = fma(rv, rv, acc[0]);
-  }
-  __shared__ double red[32];
-  block_sum<1>(acc, red);
-  double* part = a.part + (size_t)rb * RED_BLOCKS;
-  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
-  if (last_block(&a.ctr->tickets[rb * 8])) {
-    __shared__ double out[1];
-    finalize(part, 1, out);
-    if (threadIdx.x == 0) {
-      SolveState& s = a.st[rb];
-      const double rn = sqrt(out[0]);
-      s.iters += 1;
-      s.rnorm = rn / s.bnorm;
-      if (!isfinite(rn)) {
-        s.status = ST_NONFINITE;
-        mark_finished(a, s);
-      } else if (rn <= a.rtol * s.bnorm) {
-        s.converged = 1;
-        mark_finished(a, s);
-      } else if (s.iters >= a.maxit) {
-        mark_finished(a, s);
-      }
-    }
-  }
-}
-
-// ρ' = r·z ; β = ρ'/ρ ; p = z + β p is done by k_pcg_p
-__global__ void k_pcg_rz(VecArgs a, const double* __restrict__ r, const double* __restrict__ z) {
-  FDE_PDL_ENTRY();
-  if (a.ctr->active == 0) return;
-  const int rb = blockIdx.y, N = a.N;
-  if (!a.st[rb].cyc_active) return;
-  const size_t o = (size_t)rb * N;
-  double acc[1] = {0.0};
-  FDE_GRID_LOOP(e) acc[0] = fma(r[o + e], z[o + e], acc[0]);
-  __shared__ double red[32];
-  block_sum<1>(acc, red);
-  double* part = a.part + (size_t)rb * RED_BLOCKS;
-  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
-  if (last_block(&a.ctr->tickets[rb * 8])) {
-    __shared__ double out[1];
-    finalize(part, 1, out);
-    if (threadIdx.x == 0) {
-      SolveState& s = a.st[rb];
-      const double rho_new = out[0];
-      if (!(rho_new > 0.0)) {
-        s.status = isfinite(rho_new) ? ST_NOT_SPD : ST_NONFINITE;
-        mark_finished(a, s);
-      } else {
-        s.betac = rho_new / s.rho;
-        s.rho = rho_new;
-      }
-    }
-  }
-}
-
-__global__ void k_pcg_p(VecArgs a, const double* __restrict__ z, double* __restrict__ p) {
-  FDE_PDL_ENTRY();
-  if (a.ctr->active == 0) return;
-  const int rb = blockIdx.y, N = a.N;
-  if (!a.st[rb].cyc_active) return;
-  const double be = a.st[rb].betac;
-  const size_t o = (size_t)rb * N;
-  FDE_GRID_LOOP(e) p[o + e] = fma(be, p[o + e], z[o + e]);
-}
-
 // ========================================================== GMRES (a4) ====
 // init: x = 0, r = b (right) ; ref = ‖r‖ ; V0 = r/‖r‖ (done by k_gm_scale)
 // For left preconditioning the caller passes r = P⁻¹b as `src`.
@@ -837,11 +727,6 @@ __global__ void k_sub(const double* __restrict__ b, const double* __restrict__ t
   FDE_PDL_ENTRY();
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     r[e] = b[e] - t[e];
-}
-__global__ void k_scale_field(const double* __restrict__ src, const double* __restrict__ f, double* dst, int N, long long n) {
-  FDE_PDL_ENTRY();
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
-    dst[e] = src[e] * f[e % N];
 }
 
 }  // namespace fde
