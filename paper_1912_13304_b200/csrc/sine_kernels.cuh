@@ -75,6 +75,7 @@ k_sineop_lines(LineArgs a) {
   constexpr int m = GD::L, P = GD::P, RD = GD::R;
   extern __shared__ double2 smem_all[];
   if (kry_skip(a)) return;
+  FDE_PROBE(0);
   const int f = M::group(), t = M::lane();
   double2* sm = smem_all + (size_t)f * GT::SM_STRIDE;
   double2* smW = smem_all + (size_t)FPC * GT::SM_STRIDE + (size_t)f * GD::SM_STRIDE;
@@ -181,7 +182,10 @@ k_sineop_lines(LineArgs a) {
     beta5 = scr[0];
     __syncthreads();
   }
-  if ((MODE == 1 || MODE == 4) && a.yin) {  // the row pass's result streams in for the epilogue (chunk layout)
+#ifndef FDE_SINE_YIN_ASYNC
+#define FDE_SINE_YIN_ASYNC 1
+#endif
+  if (FDE_SINE_YIN_ASYNC && (MODE == 1 || MODE == 4) && a.yin) {  // the row pass's result streams in for the epilogue (chunk layout)
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
       const int e = RD * t + i - 1;
@@ -193,6 +197,7 @@ k_sineop_lines(LineArgs a) {
   }
   __syncthreads();
 
+  FDE_PROBE(1);
   // 2. DST #1 (D p̂)
   double2 vd[RD];
   dstm_pre_smem<GD, KM, 3>(vd, sm, t, a.sinm);
@@ -200,6 +205,7 @@ k_sineop_lines(LineArgs a) {
   double g0[RD], g1[RD];
   dstm_post<GD, COL, FPC>(vd, sm, scr, t, f, g0, g1);
 
+  FDE_PROBE(2);
   // 3. to the Toeplitz input layout (element e at position e, zero padded to 2m)
   __syncthreads();
 #pragma unroll
@@ -231,11 +237,13 @@ k_sineop_lines(LineArgs a) {
   }
   __syncthreads();
 
+  FDE_PROBE(3);
   // 5. DST #2
   dstm_pre_smem<GD, KM, 3>(vd, sm, t, a.sinm);
   dif_chain<GD, -1, false>(vd, sm, t, twd);
   dstm_post<GD, COL, FPC>(vd, sm, scr, t, f, g0, g1);
 
+  FDE_PROBE(4);
   // 6. epilogue
   if (MODE == 4) {
     // columns, recurrence body: w = ν ẑ + yin + op, q̂ = w + β q̂, p̂ = ẑ + β p̂
@@ -266,7 +274,7 @@ k_sineop_lines(LineArgs a) {
     }
   } else if (MODE == 1) {
     // columns: this lane owns rows e = RD t + i - 1 of its two columns
-    if (a.yin) cp_async_wait_all();
+    if (FDE_SINE_YIN_ASYNC && a.yin) cp_async_wait_all();
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
       const int e = RD * t + i - 1;
@@ -274,14 +282,16 @@ k_sineop_lines(LineArgs a) {
       if (v0) {
         const long long o = A0.base + (long long)e * A0.stride;
         const double pv = a.kf.p[o];
-        const double qv = fma(a.nu, pv, g0[i] + (a.yin ? smW[GD::swz(e)].x : 0.0));
+        const double yv = a.yin ? (FDE_SINE_YIN_ASYNC ? smW[GD::swz(e)].x : a.yin[o]) : 0.0;
+        const double qv = fma(a.nu, pv, g0[i] + yv);
         a.y[o] = qv;
         acc[0] = fma(pv, qv, acc[0]);
       }
       if (v1) {
         const long long o = A1.base + (long long)e * A1.stride;
         const double pv = a.kf.p[o];
-        const double qv = fma(a.nu, pv, g1[i] + (a.yin ? smW[GD::swz(e)].y : 0.0));
+        const double yv = a.yin ? (FDE_SINE_YIN_ASYNC ? smW[GD::swz(e)].y : a.yin[o]) : 0.0;
+        const double qv = fma(a.nu, pv, g1[i] + yv);
         a.y[o] = qv;
         acc[0] = fma(pv, qv, acc[0]);
       }
@@ -344,6 +354,7 @@ k_sineop_lines(LineArgs a) {
   } else if (MODE == 3) {
     kry_reduce_finalize(a.kf, acc);
   }
+  FDE_PROBE(5);
   if (MODE != 5 || !a.persist) break;
   __syncthreads();  // persistent 1D solve: the next body reuses sm and reads this body's writes
   }

@@ -1,0 +1,39 @@
+"""Per-CTA phase timing of the sine-domain PCG line kernels (-DFDE_PROBES
+build, FDE_GRAPH=0): markers 0 start, 1 staged, 2 DST#1, 3 Toeplitz,
+4 DST#2, 5 end (%globaltimer)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["FDE_LIB"] = os.path.join(ROOT, "paper_1912_13304_b200", "libfde_probe.so")
+os.environ["FDE_GRAPH"] = "0"
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+from paper_1912_13304_b200 import fde  # noqa: E402
+
+fde.lib.fde_debug_probes.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+p = W.config(5, n=1023)
+h = fde.Fde.from_problem(p, stream=torch.cuda.current_stream().cuda_stream)
+b = torch.from_numpy(p.rhs.copy()).cuda()
+x = torch.zeros_like(b)
+buf = np.zeros((8, 2048, 8), dtype=np.uint64)
+for _ in range(2):
+    fde.lib.fde_debug_probes(buf.ctypes.data, buf.nbytes)
+    h.pcg(b, x, 1e-10, 2)
+    torch.cuda.synchronize()
+    fde.lib.fde_debug_probes(buf.ctypes.data, buf.nbytes)
+for s, nm in ((4, "sine_op_rows"), (5, "sine_op_cols")):
+    bb = buf[s].astype(np.int64)
+    used = bb[:, 0] > 0
+    bb = bb[used]
+    t0 = bb[:, 0].min()
+    rel = (bb - t0) / 1e3
+    print("%-14s CTAs %4d start spread %.2f us end %.2f us" % (nm, used.sum(), rel[:, 0].max(), rel[:, 5].max()))
+    for i in range(5):
+        d = rel[:, i + 1] - rel[:, i]
+        print("   phase %d->%d  median %.2f  max %.2f us" % (i, i + 1, np.median(d), d.max()))
