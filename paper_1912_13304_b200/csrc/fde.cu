@@ -1377,7 +1377,8 @@ fde_status run_gmres(fde_handle h, const double* b, double* x, double rtol, int 
 
   // one graph launch per solve: WHILE(some RHS unfinished) { one restart cycle }
   const int max_cycles = maxit / restart + 2;
-  if (!h->g_gm || h->g_gm_restart != restart || h->g_gm_left != left || h->g_rtol != rtol || h->g_maxit != maxit) {
+  if (!h->no_graph && (!h->g_gm || h->g_gm_restart != restart || h->g_gm_left != left || h->g_rtol != rtol ||
+                      h->g_maxit != maxit)) {
     if (h->g_gm) { cudaGraphExecDestroy(h->g_gm); h->g_gm = nullptr; }
     h->g_gm_nodes = build_while_graph(h, &h->g_gm, max_cycles, [&] { gmres_cycle(h, va, restart, left); });
     h->g_gm_restart = restart;
@@ -1385,14 +1386,21 @@ fde_status run_gmres(fde_handle h, const double* b, double* x, double rtol, int 
     h->g_rtol = rtol;
     h->g_maxit = maxit;
   }
-  FDE_CUDA(cudaGraphLaunch(h->g_gm, h->st));
+  if (h->no_graph) {  // FDE_GRAPH=0 (profilers): the same cycle from the host
+    for (int c = 0; c < max_cycles; ++c) {
+      gmres_cycle(h, va, restart, left);
+      if (read_active(h) == 0) break;
+    }
+  } else {
+    FDE_CUDA(cudaGraphLaunch(h->g_gm, h->st));
+  }
   if (is_device_ptr(x)) {
     FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
   } else {
     FDE_CUDA(cudaMemcpyAsync(x, h->kx, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   }
   const fde_status ws = worst_status(h, st, false);
-  h->launches += (long long)read_loops(h) * h->g_gm_nodes;
+  if (!h->no_graph) h->launches += (long long)read_loops(h) * h->g_gm_nodes;
   return ws;
 }
 

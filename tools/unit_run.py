@@ -16,6 +16,7 @@ ap.add_argument("--n", type=int, default=1023)
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--pcg", action="store_true", help="also run one fde_pcg solve")
+ap.add_argument("--gmres", type=int, default=0, help="also run one fde_gmres solve with this maxit")
 a = ap.parse_args()
 p = W.config(a.cfg, n=a.n, batch=a.batch)
 h = fde.Fde.from_problem(p, stream=torch.cuda.current_stream().cuda_stream)
@@ -28,5 +29,8 @@ for _ in range(a.reps):
 if a.pcg:
     xs = torch.zeros_like(x)
     print(h.pcg(x, xs, p.rtol, p.maxit))
+if a.gmres:
+    xs = torch.zeros_like(x)
+    print(h.gmres(x, xs, p.rtol, p.restart, a.gmres))
 torch.cuda.synchronize()
 print("ok", float(y.norm()), float(z.norm()))
