@@ -27,6 +27,8 @@ SURVEY.md §8(c) (R-numbers refer to DESIGN.md §3):
       d̄ = mean((d₊+d₋)/2), ē = mean((e₊+e₋)/2).
   R14 2D y-term weight `ywt` (BASELINE: 1; the paper's CN system: s/r).
   R15 D_N = (D₊+D₋+E₊+E₋)/4 uses the unweighted E±.
+  R19 P_tri = the three main diagonals of M (1D), solved by the
+      Thomas algorithm written out.
 
 Pinning (tests/test_oracle_*.py): each function below is checked against
 values the paper prints (Tables 1-4, tests/golden/), closed forms, identities
@@ -44,7 +46,7 @@ __all__ = [
     "grunwald_g", "wsgd_w", "toeplitz_T", "symbol_g", "symbol_w", "symbol_p",
     "symbol_q", "symbol_F", "theta_grid", "sine_matrix", "sine_mode", "tau_matrix",
     "System", "pcg", "gmres", "lu_solve", "cond2",
-    "PREC_NONE", "PREC_TAU", "PREC_TAU_D", "PREC_TAU_DSYM", "PREC_TILDE",
+    "PREC_NONE", "PREC_TAU", "PREC_TAU_D", "PREC_TAU_DSYM", "PREC_TILDE", "PREC_TRI", "thomas",
     "example1_matrices", "example1_run", "example2_matrices", "example2_run",
 ]
 
@@ -167,7 +169,27 @@ def tau_matrix(samples: np.ndarray) -> np.ndarray:
 # L2/L3: the discrete system and the preconditioners
 # ---------------------------------------------------------------------------
 
-PREC_NONE, PREC_TAU, PREC_TAU_D, PREC_TAU_DSYM, PREC_TILDE = 0, 1, 2, 3, 4
+PREC_NONE, PREC_TAU, PREC_TAU_D, PREC_TAU_DSYM, PREC_TILDE, PREC_TRI = 0, 1, 2, 3, 4, 5
+
+
+def thomas(sub: np.ndarray, diag: np.ndarray, sup: np.ndarray, d: np.ndarray) -> np.ndarray:
+    """Solve the tridiagonal system (sub_i x_{i-1} + diag_i x_i + sup_i x_{i+1}
+    = d_i) by the Thomas algorithm (forward elimination, back substitution),
+    written out; sub_0 and sup_{n-1} are ignored."""
+    n = len(diag)
+    c = np.empty(n)
+    g = np.empty(n)
+    c[0] = sup[0] / diag[0]
+    g[0] = d[0] / diag[0]
+    for i in range(1, n):
+        den = diag[i] - sub[i] * c[i - 1]
+        c[i] = sup[i] / den if i < n - 1 else 0.0
+        g[i] = (d[i] - sub[i] * g[i - 1]) / den
+    x = np.empty(n)
+    x[n - 1] = g[n - 1]
+    for i in range(n - 2, -1, -1):
+        x[i] = g[i] - c[i] * x[i + 1]
+    return x
 
 
 class System:
@@ -288,6 +310,9 @@ class System:
         r = np.asarray(r, dtype=np.float64)
         if kind == PREC_NONE:
             return r.copy()
+        if kind == PREC_TRI:   # P_tri = tridiag(M) (R19), 1D
+            sub, diag, sup = self.tridiagonal()
+            return thomas(sub, diag, sup, r)
         F = self.symbol_samples(cx, cy).reshape(-1)
         if kind == PREC_TILDE:
             F = self.D() * F
@@ -301,8 +326,23 @@ class System:
         t = t / F
         return post * self.sine_apply(t)
 
+    def tridiagonal(self):
+        """The three main diagonals of M (1D): M_{i,i-1}, M_{i,i},
+        M_{i,i+1} read off the dense operator's definition (sub_0 = sup_{n-1} = 0)."""
+        n = self.n
+        Md = self.nu * np.eye(n) + np.diag(self.dp) @ self.Ta + np.diag(self.dm) @ self.Ta.T
+        diag = np.diag(Md).copy()
+        sub = np.zeros(n)
+        sup = np.zeros(n)
+        sub[1:] = np.diag(Md, -1)
+        sup[:-1] = np.diag(Md, 1)
+        return sub, diag, sup
+
     def prec_dense(self, kind: int, cx: float = 1.0, cy: float = 1.0) -> np.ndarray:
         """The preconditioner P itself as a dense matrix (small n; κ pins)."""
+        if kind == PREC_TRI:
+            sub, diag, sup = self.tridiagonal()
+            return np.diag(diag) + np.diag(sub[1:], -1) + np.diag(sup[:-1], 1)
         F = self.symbol_samples(cx, cy).reshape(-1)
         if kind == PREC_TILDE:
             F = self.D() * F

@@ -380,3 +380,51 @@ def test_matvec_entries_and_sine_modes():
     F = s.symbol_samples(0.7, 1.1)
     assert np.allclose(s.prec_solve(md, O.PREC_TAU, 0.7, 1.1), md / F[6, 2], atol=1e-14)
     assert np.allclose(O.sine_mode(12, 5), O.sine_matrix(12)[:, 4])
+
+
+TABLE2_TRI = load_golden("table2_ptri.txt")
+
+
+def test_thomas_against_lu():
+    """The written-out Thomas algorithm equals Gaussian elimination on random
+    diagonally dominant tridiagonal systems (brute force)."""
+    rng = np.random.default_rng(4)
+    for n in (1, 2, 5, 40):
+        sub, sup = rng.standard_normal(n), rng.standard_normal(n)
+        diag = 4.0 + np.abs(rng.standard_normal(n))
+        sub[0] = sup[-1] = 0.0
+        A = np.diag(diag) + np.diag(sub[1:], -1) + np.diag(sup[:-1], 1)
+        d = rng.standard_normal(n)
+        assert np.allclose(O.thomas(sub, diag, sup, d), O.lu_solve(A, d), rtol=1e-13, atol=1e-13)
+
+
+def test_tridiagonal_part_closed_form():
+    """tridiag(M) of M = νI + D₊T + D₋Tᵀ: diagonal ν + α(d₊+d₋),
+    sub-diagonal −(d₊ g₂ + d₋), super-diagonal −(d₊ + d₋ g₂) with g₂ = α(α−1)/2."""
+    ex = W.example1(1.5, 15)
+    s = O.example1_matrices(ex, 1.5, 15)
+    sub, diag, sup = s.tridiagonal()
+    g2 = 1.5 * 0.5 / 2
+    assert np.allclose(diag, ex["nu"] + 1.5 * (ex["dp"] + ex["dm"]), rtol=1e-14)
+    assert np.allclose(sub[1:], -(ex["dp"][1:] * g2 + ex["dm"][1:]), rtol=1e-14)
+    assert np.allclose(sup[:-1], -(ex["dp"][:-1] + ex["dm"][:-1] * g2), rtol=1e-14)
+
+
+@pytest.mark.parametrize("row", TABLE2_TRI, ids=lambda r: "a%.1f-n%d" % (r[0], r[1]))
+def test_table2_ptri_kappa(row):
+    alpha, n1 = row[0], int(row[1])
+    n = n1 - 1
+    ex = W.example1(alpha, n)
+    s = O.example1_matrices(ex, alpha, n)
+    M = s.dense()
+    P = s.prec_dense(O.PREC_TRI)
+    kappa = O.cond2(np.linalg.solve(P, M))
+    assert round(kappa, 1) == row[3], kappa
+
+
+@pytest.mark.parametrize("row", [r for r in TABLE2_TRI if r[1] <= 256], ids=lambda r: "a%.1f-n%d" % (r[0], r[1]))
+def test_table2_ptri_iterations(row):
+    alpha, n1 = row[0], int(row[1])
+    ex = W.example1(alpha, n1 - 1)
+    it, _ = O.example1_run(ex, alpha, n1 - 1, O.PREC_TRI)
+    assert abs(it - row[2]) <= 0.15, it
