@@ -22,6 +22,7 @@
  *   FDE_PREC_TAU_DSYM P = D^{1/2} τ(F) D^{1/2}   (P:L313 as printed)
  *   FDE_PREC_TILDE    P̃ = S diag(D_j·F(θ_j)) S  (1D only; the alternative of P:L606,
  *                                          Table 2; reading R7)
+ *   FDE_PREC_TRI      P_tri = tridiag(A)     (1D only; Table 2; GMRES only)
  *   D = (D₊+D₋)/2 in 1D, (D₊+D₋+E₊+E₋)/4 in 2D.
  *
  * Layout: every vector is fp64, C-contiguous, x-fastest: element
@@ -68,7 +69,8 @@ typedef enum {
   FDE_PREC_TAU = 1,
   FDE_PREC_TAU_D = 2,
   FDE_PREC_TAU_DSYM = 3,
-  FDE_PREC_TILDE = 4
+  FDE_PREC_TILDE = 4,
+  FDE_PREC_TRI = 5
 } fde_prec;
 
 typedef struct {
@@ -85,7 +87,7 @@ typedef struct {
   const double* dm_field;
   const double* ep_field;
   const double* em_field;
-  int32_t prec;     /* fde_prec (FDE_PREC_TILDE needs dims == 1) */
+  int32_t prec;     /* fde_prec (FDE_PREC_TILDE and FDE_PREC_TRI need dims == 1, n <= 4095) */
   double cx, cy;    /* τ weights; <= 0 selects: TAU -> mean((d₊+d₋)/2), mean((e₊+e₋)/2)
                        (R12); TAU_D/TAU_DSYM -> 1 */
   double ywt;       /* weight of the 2D y-term (the paper's s/r); <= 0 -> 1 */

@@ -24,6 +24,7 @@
 #include "line_kernels.cuh"
 #include "sine_kernels.cuh"
 #include "dense_kernels.cuh"
+#include "tri_kernels.cuh"
 
 using namespace fde;
 
@@ -248,6 +249,7 @@ struct fde_handle_s {
   // tables
   bool dense = false;                 // direct path (dense_kernels.cuh): n+1 not a supported power of two
   double *coef_x = nullptr, *coef_y = nullptr, *sint = nullptr;
+  double *tri_sub = nullptr, *tri_diag = nullptr, *tri_sup = nullptr;  // FDE_PREC_TRI
   double2* tw = nullptr;
   double2* twp = nullptr;
   double2* twpm = nullptr;
@@ -618,6 +620,15 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate, const Kry
       kpost.mode &= (KM_RZ | KM_GATE);
     }
   }
+  if (h->d.prec == FDE_PREC_TRI) {  // P_tri⁻¹ r by parallel cyclic reduction (tri_kernels.cuh)
+    if (kf) throw FdeFail{FDE_ERR_UNSUPPORTED, "FDE_PREC_TRI is available with fde_gmres and fde_tau_apply"};
+    const int n = h->n;
+    const double *sb = h->tri_sub, *dg = h->tri_diag, *sp = h->tri_sup;
+    launch_named(h, "tri_pcr", [&] {
+      launch_k(h->st, k_tri_pcr, dim3(1, h->batch), TRI_THREADS, (size_t)4 * n * sizeof(double), sb, dg, sp, r, z, n, gate);
+    });
+    return;
+  }
   if (h->d.prec == FDE_PREC_NONE) {
     if (kf) {
       const KryFuse k = *kf;
@@ -802,7 +813,22 @@ void build(fde_handle h, const fde_desc* d) {
 
   // preconditioner tables
   const int prec = d->prec;
-  if (prec != FDE_PREC_NONE) {
+  if (prec == FDE_PREC_TRI) {
+    // tridiag(M): M_ii = ν - c_1 (d₊+d₋), M_{i,i-1} = -(d₊ c_2 + d₋ c_0), M_{i,i+1} = -(d₊ c_0 + d₋ c_2)
+    // with [T]_{ij} = -c_{i-j+1} (c = g or w)
+    const std::vector<double> co = stencil_coeffs(d->alpha, 2, d->stencil);
+    std::vector<double> sb(n), dg(n), sp(n);
+    for (int i = 0; i < n; ++i) {
+      dg[i] = d->nu - co[1] * (dp[i] + dm[i]);
+      sb[i] = -(dp[i] * co[2] + dm[i] * co[0]);
+      sp[i] = -(dp[i] * co[0] + dm[i] * co[2]);
+    }
+    h->tri_sub = h->upload(sb);
+    h->tri_diag = h->upload(dg);
+    h->tri_sup = h->upload(sp);
+    const int smem = 4 * n * (int)sizeof(double);
+    if (smem > 48 * 1024) FDE_CUDA(cudaFuncSetAttribute(k_tri_pcr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  } else if (prec != FDE_PREC_NONE) {
     double cx = d->cx, cy = d->cy;
     if (prec == FDE_PREC_TAU) {
       if (!(cx > 0.0)) {  // R12: mean((d+ + d-)/2)
@@ -910,8 +936,10 @@ void validate(const fde_desc* d) {
   coef(d->dp);
   coef(d->dm);
   if (d->dims == 2) { coef(d->ep); coef(d->em); }
-  if (d->prec < FDE_PREC_NONE || d->prec > FDE_PREC_TILDE) bad("unknown prec kind");
+  if (d->prec < FDE_PREC_NONE || d->prec > FDE_PREC_TRI) bad("unknown prec kind");
   if (d->prec == FDE_PREC_TILDE && d->dims != 1) bad("FDE_PREC_TILDE is defined in 1D only (P:L606)");
+  if (d->prec == FDE_PREC_TRI && (d->dims != 1 || d->n > TRI_THREADS * TRI_PER_THREAD))
+    bad("FDE_PREC_TRI is defined in 1D only (P:L605), n <= 4096");
   if (!std::isfinite(d->cx) || !std::isfinite(d->cy) || !std::isfinite(d->ywt)) bad("cx, cy, ywt must be finite");
   if ((long long)d->n * (d->dims == 2 ? d->n : 1) * d->batch > (1LL << 31)) bad("problem too large");
 }

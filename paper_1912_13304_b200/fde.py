@@ -30,7 +30,7 @@ FDE_ERR_BREAKDOWN = 7
 FDE_ERR_NONFINITE = 8
 FDE_ERR_NOT_CONVERGED = 9
 
-FDE_PREC_NONE, FDE_PREC_TAU, FDE_PREC_TAU_D, FDE_PREC_TAU_DSYM, FDE_PREC_TILDE = 0, 1, 2, 3, 4
+FDE_PREC_NONE, FDE_PREC_TAU, FDE_PREC_TAU_D, FDE_PREC_TAU_DSYM, FDE_PREC_TILDE, FDE_PREC_TRI = 0, 1, 2, 3, 4, 5
 
 
 class fde_desc(ctypes.Structure):

@@ -8,6 +8,7 @@ import pytest
 
 import oracle as O
 import workloads as W
+from conftest import load_golden
 from test_gpu_ops import oracle_system, oracle_weights, relerr
 
 pytestmark = pytest.mark.gpu
@@ -386,3 +387,42 @@ def test_host_pointer_solves_match_device_solves(torch_cuda):
             h.gmres(np.ascontiguousarray(p.rhs), xh)
         assert np.array_equal(x.cpu().numpy(), xh)
         h.close()
+
+
+@pytest.mark.parametrize("n,alpha", [(63, 1.2), (127, 1.5), (100, 1.8), (4095, 1.5)])
+def test_tri_operator_parity(torch_cuda, n, alpha):
+    """P_tri⁻¹ r (parallel cyclic reduction on the GPU) against the
+    oracle's written-out Thomas algorithm, Example 1 coefficients."""
+    from paper_1912_13304_b200 import fde
+    ex = W.example1(alpha, n)
+    s = O.example1_matrices(ex, alpha, n)
+    h = fde.Fde(n, 1, alpha, nu=ex["nu"], dp_field=ex["dp"], dm_field=ex["dm"], prec=W.PREC_TRI, batch=2)
+    x = np.random.default_rng(6).standard_normal((2, n))
+    z = np.zeros_like(x)
+    h.tau_apply(x, z)
+    for b in range(2):
+        assert relerr(z[b], s.prec_solve(x[b], O.PREC_TRI)) <= 1e-12
+    with pytest.raises(fde.FdeError):
+        h.pcg(x, z)
+    h.close()
+
+
+def test_paper_table2_ptri_iterations_on_gpu(torch_cuda):
+    """Example 1 with P_tri: Table 2's printed iteration counts
+     at n1+1 = 64 and 128, every GMRES solve on the GPU."""
+    from paper_1912_13304_b200 import fde
+    rows = [r for r in load_golden("table2_ptri.txt") if r[1] <= 128]
+    for alpha, n1, printed, _ in rows:
+        n = int(n1) - 1
+        ex = W.example1(alpha, n)
+        h = fde.Fde(n, 1, alpha, nu=ex["nu"], dp_field=ex["dp"], dm_field=ex["dm"], prec=W.PREC_TRI)
+        u = ex["u0"].copy()
+        its = 0
+        for m_ in range(1, ex["M"] + 1):
+            b = (ex["nu"] * u + ex["h"] ** alpha * ex["f"](m_ * ex["ht"]))[None, :]
+            x = np.zeros_like(b)
+            st, stats = h.gmres(np.ascontiguousarray(b), x, 1e-7, 64, 64, left=True)
+            its += stats[0]["iters"]
+            u = x[0]
+        h.close()
+        assert abs(its / ex["M"] - printed) <= 0.15, (alpha, n1, its / ex["M"])

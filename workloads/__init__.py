@@ -25,7 +25,7 @@ from typing import Optional
 import numpy as np
 
 # prec kinds (mirrors include/fde.h; plain integers, no arithmetic)
-PREC_NONE, PREC_TAU, PREC_TAU_D, PREC_TAU_DSYM, PREC_TILDE = 0, 1, 2, 3, 4
+PREC_NONE, PREC_TAU, PREC_TAU_D, PREC_TAU_DSYM, PREC_TILDE, PREC_TRI = 0, 1, 2, 3, 4, 5
 
 
 @dataclass
