@@ -218,9 +218,9 @@ struct LaunchCfgM {
 // sine-domain operator kernels (sine_kernels.cuh)
 template <int KM, bool COL, int MODE>
 struct LaunchCfgS {
-  using GT = FftGeom<KM + 1, 4>;
-  static constexpr int P = 1 << (KM - 3);
-  static constexpr int SPG = GT::SM_STRIDE * 16 + ((MODE == 1 || MODE == 4) ? FftGeom<KM, 3>::SM_STRIDE * 16 : 0);
+  using GT = FftGeom<KM + 1, sine_kd(KM) + 1>;
+  static constexpr int P = 1 << (KM - sine_kd(KM));
+  static constexpr int SPG = GT::SM_STRIDE * 16 + ((MODE == 1 || MODE == 4) ? FftGeom<KM, sine_kd(KM)>::SM_STRIDE * 16 : 0);
   static constexpr int BY_SMEM = (200 * 1024) / SPG > 0 ? (200 * 1024) / SPG : 1;
   static constexpr int BY_THR = 512 / P > 0 ? 512 / P : 1;
 #ifndef FDE_SINE_COL_FPC
@@ -253,6 +253,7 @@ struct fde_handle_s {
   double2* tw = nullptr;
   double2* twp = nullptr;
   double2* twpm = nullptr;
+  double2 *twps_d = nullptr, *twps_t = nullptr;  // per-pass tables of the sine kernels' FFTs (FDE_SINE_KD)
   double* sinm = nullptr;
   double2 *mu_x = nullptr, *mu_y = nullptr;
   double2 *mus_x = nullptr, *mus_y = nullptr;  // sine-domain μ_s (constant directions; sine_kernels.cuh)
@@ -373,8 +374,11 @@ void launch_dstm_k(fde_handle h, const LineArgs& a) {
 }
 
 template <int KM, bool COL, int MODE>
-void launch_sineop_k(fde_handle h, const LineArgs& a) {
+void launch_sineop_k(fde_handle h, const LineArgs& a0) {
   using C = LaunchCfgS<KM, COL, MODE>;
+  LineArgs a = a0;
+  a.twpm = h->twps_d;
+  a.twp = h->twps_t;
   auto kern = k_sineop_lines<KM, COL, C::FPC, MODE>;
   static bool attr = false;
   if (!attr) {
@@ -721,6 +725,9 @@ void build(fde_handle h, const fde_desc* d) {
     // per-pass twiddle tables of the length-L (Toeplitz) and length-m (DST) FFTs
     h->twp = h->upload(pass_twiddles_host(h->K, KR));
     h->twpm = h->upload(pass_twiddles_host(h->K - 1, KRM));
+    const int kd = sine_kd(h->K - 1);
+    h->twps_d = kd == KRM ? h->twpm : h->upload(pass_twiddles_host(h->K - 1, kd));
+    h->twps_t = kd + 1 == KR ? h->twp : h->upload(pass_twiddles_host(h->K, kd + 1));
     std::vector<double> sv(m);
     for (int j = 0; j < m; ++j) sv[j] = std::sin(M_PI * (double)std::min(j, m - j) / (double)m);  // sin(πj/m)
     h->sinm = h->upload(sv);

@@ -18,6 +18,17 @@
 
 namespace fde {
 
+// log2 points per thread of the sine kernels' DST FFTs (the Toeplitz FFTs use
+// one more, so both share one thread layout): measured on the B200, 4 points
+// (more threads per line) win up to m = 512, 8 points from m = 1024 on.
+__host__ __device__ constexpr int sine_kd(int KM) {
+#ifdef FDE_SINE_KD
+  return FDE_SINE_KD;
+#else
+  return KM <= 9 ? 2 : 3;
+#endif
+}
+
 // CTA-wide fixed-order sum of acc[0..2]; the result is valid in thread 0.
 // scr: >= 3*32 doubles of shared memory; ends with a barrier.
 __device__ __forceinline__ void block_reduce3(double (&acc)[3], double* scr) {
@@ -65,11 +76,11 @@ __device__ __forceinline__ double symbol_at(const LineArgs& a, int l, int e) {
 // MODE 2: 1D:            p̂ = r̂/F + β p̂, y = q̂ = ν p̂ + (S T̃ S) p̂, partial p̂·q̂
 // a.x = r̂ (MODE 0/2) or p̂ (MODE 1); a.kf.p = p̂; a.mu = the sine-domain μ_s.
 template <int KM, bool COL, int FPC, int MODE>
-__global__ void __launch_bounds__(FPC * (1 << (KM - 3)), min_blocks_for(FPC * (1 << (KM - 3))))
+__global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), min_blocks_for(FPC * (1 << (KM - sine_kd(KM)))))
 k_sineop_lines(LineArgs a) {
   FDE_PDL_ENTRY();
-  using GD = FftGeom<KM, 3>;      // DST: length-m FFT, 8 points per thread
-  using GT = FftGeom<KM + 1, 4>;  // Toeplitz: length-2m FFT, 16 points per thread
+  using GD = FftGeom<KM, sine_kd(KM)>;           // DST: length-m FFT, 2^KD points per thread
+  using GT = FftGeom<KM + 1, sine_kd(KM) + 1>;   // Toeplitz: length-2m FFT, 2^(KD+1) points per thread
   static_assert(GD::P == GT::P, "one thread layout for both transforms");
   using M = LineMap<GD, COL, FPC>;
   constexpr int m = GD::L, P = GD::P, RD = GD::R;
@@ -200,7 +211,7 @@ k_sineop_lines(LineArgs a) {
   FDE_PROBE(1);
   // 2. DST #1 (D p̂)
   double2 vd[RD];
-  dstm_pre_smem<GD, KM, 3>(vd, sm, t, a.sinm);
+  dstm_pre_smem<GD, KM, sine_kd(KM)>(vd, sm, t, a.sinm);
   dif_chain<GD, -1, false>(vd, sm, t, twd);
   double g0[RD], g1[RD];
   dstm_post<GD, COL, FPC>(vd, sm, scr, t, f, g0, g1);
@@ -227,7 +238,7 @@ k_sineop_lines(LineArgs a) {
   // 4. T̃ via the circulant embedding (μ_s carries d or e, 1/L and 1/(2m))
   dif_chain<GT, -1, true>(v, sm, t, twt);
 #pragma unroll
-  for (int q = 0; q < GT::R; ++q) v[q] = c_mul(v[q], a.mu[(t << 4) | q]);
+  for (int q = 0; q < GT::R; ++q) v[q] = c_mul(v[q], a.mu[(t << GT::k) | q]);
   dit_chain<GT, +1>(v, sm, t, twt);
   __syncthreads();
 #pragma unroll
@@ -239,7 +250,7 @@ k_sineop_lines(LineArgs a) {
 
   FDE_PROBE(3);
   // 5. DST #2
-  dstm_pre_smem<GD, KM, 3>(vd, sm, t, a.sinm);
+  dstm_pre_smem<GD, KM, sine_kd(KM)>(vd, sm, t, a.sinm);
   dif_chain<GD, -1, false>(vd, sm, t, twd);
   dstm_post<GD, COL, FPC>(vd, sm, scr, t, f, g0, g1);
 
