@@ -200,6 +200,20 @@ def run_reference(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------- multi-rank
+def reduce_over_ranks(ms: float, iters: int, device):
+    """Replicas only: the job's time is the MAX of the ranks'
+    device times, its work the SUM of their iterations. Collective on the
+    default process group (NCCL on the GPU box; gloo in the CPU tests)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    k = torch.tensor([float(iters)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(k, op=dist.ReduceOp.SUM)
+    return float(t.item()), int(k.item())
+
+
 # ----------------------------------------------------------------- product arm
 def run_fde(args, rank, world, local_rank):
     import torch
@@ -242,11 +256,7 @@ def run_fde(args, rank, world, local_rank):
     clocks = clk.stop()
     ms = sum(a.elapsed_time(c) for a, c in ev)
     if world > 1:
-        t = torch.tensor([ms, float(iters)], dtype=torch.float64, device=dev)
-        tmax = t[:1].clone()
-        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
-        ms, iters = float(tmax.item()), int(t[1].item())
+        ms, iters = reduce_over_ranks(ms, iters, dev)
     value = iters / (ms / 1e3)
 
     # e2e: the same solve through the C ABI from pinned HOST buffers
@@ -266,11 +276,7 @@ def run_fde(args, rank, world, local_rank):
         e_ms += e0.elapsed_time(e1)
         e_it += sum(s["iters"] for s in stats)
     if world > 1:
-        t = torch.tensor([e_ms, float(e_it)], dtype=torch.float64, device=dev)
-        tm = t[:1].clone()
-        torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
-        e_ms, e_it = float(tm.item()), int(t[1].item())
+        e_ms, e_it = reduce_over_ranks(e_ms, e_it, dev)
     e2e = {"value": e_it / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(bn.nbytes),
            "d2h_bytes_per_step": int(xn.nbytes), "path": "fde_pcg with pinned host b, x (library-staged copies)"}
 
