@@ -286,6 +286,7 @@ struct fde_handle_s {
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
   bool no_graph = false;            // env FDE_GRAPH=0: host-driven loop (for profilers)
+  int sine_pitch = 0;               // row pitch of the sine-domain PCG's internal 2D vectors (n+1)
   bool sine_legacy = true;          // 3-kernel sine-domain body; env FDE_SINE_BODY=2: the recurrence body (A/B)
   bool sine1d_graph = false;        // env FDE_SINE1D=graph: 1D PCG per-iteration graph instead of one persistent kernel
   std::vector<void*> allocs;
@@ -379,6 +380,7 @@ void launch_sineop_k(fde_handle h, const LineArgs& a0) {
   LineArgs a = a0;
   a.twpm = h->twps_d;
   a.twp = h->twps_t;
+  a.pitch = h->sine_pitch;
   auto kern = k_sineop_lines<KM, COL, C::FPC, MODE>;
   static bool attr = false;
   if (!attr) {
@@ -900,7 +902,8 @@ void build(fde_handle h, const fde_desc* d) {
     }
   }
 
-  const size_t ve = h->vec_elems();
+  h->sine_pitch = h->dims == 2 ? m : n;   // m = n+1: even on the FFT path (16-byte aligned rows)
+  const size_t ve = std::max(h->vec_elems(), (size_t)h->batch * (h->dims == 2 ? (size_t)n * m : (size_t)n));
   if (h->var_x || h->var_y) h->zscr = h->dalloc<double2>((size_t)h->batch * (m / 2 + 64) * L);
   h->wx = h->dalloc<double>(ve);
   h->t1 = h->dalloc<double>(ve);
@@ -1046,13 +1049,14 @@ __global__ void k_reactivate(Counters* c, SolveState* s, int batch) {
 
 void ensure_krylov(fde_handle h, int nvecV) {
   const size_t ve = h->vec_elems();
+  const size_t vs = std::max(ve, (size_t)h->batch * (h->dims == 2 ? (size_t)h->n * h->m : (size_t)h->n));  // sine pitch
   if (!h->kx) {
-    h->kx = h->dalloc<double>(ve);
+    h->kx = h->dalloc<double>(vs);
     h->kb = h->dalloc<double>(ve);
-    h->kr = h->dalloc<double>(ve);
+    h->kr = h->dalloc<double>(vs);
     h->kz = h->dalloc<double>(ve);
-    h->kp = h->dalloc<double>(ve);
-    h->kq = h->dalloc<double>(ve);
+    h->kp = h->dalloc<double>(vs);
+    h->kq = h->dalloc<double>(vs);
     h->kpart = h->dalloc<double>((size_t)h->batch * 3 * KPMAX);
   }
   if (nvecV > h->V_cols) {
@@ -1255,7 +1259,8 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     return e ? std::atoi(e) : 592;
   }();
   const int gx = dims == 2 ? std::min(n, xr_grid) : 64;
-  launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr, dim3(gx, h->batch), 256, 0, kv, n, dims, Fx, Fy); });
+  const int pitch = h->sine_pitch;
+  launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr, dim3(gx, h->batch), 256, 0, kv, n, dims, Fx, Fy, pitch); });
 }
 
 fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, int maxit, fde_stats* st) {
@@ -1264,13 +1269,22 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   const double* bd = stage_in(h, b, h->hin, bh);
   launch_k(h->st, k_reset_counters, 1, 32, 0, h->ctr, h->sst, h->batch);
   h->launches++;
-  op_dst_all(h, bd, h->kr, 0.0);  // r̂ = b̂ (unnormalised)
+  if (h->dims == 2) {  // r̂ = b̂ (unnormalised), into the internal row pitch
+    op_dst_all(h, bd, h->t2, 0.0);
+    const double* src = h->t2;
+    double* dst = h->kr;
+    const int n = h->n, pp = h->sine_pitch;
+    launch_named(h, "repitch", [&] { launch_k(h->st, k_repitch, dim3(std::min(n, 1024), h->batch), 256, 0, src, dst, n, n, pp); });
+  } else {
+    op_dst_all(h, bd, h->kr, 0.0);  // r̂ = b̂ (unnormalised)
+  }
   KryFuse kf = make_kf(h, rtol, maxit);
   const double* Fx = h->Fx;
   const double* Fy = h->dims == 2 ? h->Fy : nullptr;
   const int n = h->n, dims = h->dims;
   const int gx = dims == 2 ? std::min(n, KPMAX) : 64;
-  launch_named(h, "sine_init", [&] { launch_k(h->st, k_sine_init, dim3(gx, h->batch), 256, 0, kf, n, dims, Fx, Fy); });
+  const int pitch = h->sine_pitch;
+  launch_named(h, "sine_init", [&] { launch_k(h->st, k_sine_init, dim3(gx, h->batch), 256, 0, kf, n, dims, Fx, Fy, pitch); });
   const bool persist1d = h->dims == 1 && !h->sine1d_graph;
   if (persist1d) {
     // 1D: the whole solve in ONE kernel, one CTA per RHS (the line fits in a
@@ -1304,7 +1318,15 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   // x = (S⊗S) x̂ = (D⊗D) x̃ / (2m)^dims
   const double s = 1.0 / (2.0 * h->m);
   const bool xdev = is_device_ptr(x);
-  op_dst_all(h, h->kx, xdev ? x : h->hout, h->dims == 2 ? s * s : s);
+  if (h->dims == 2) {
+    const double* src = h->kx;
+    double* dst = h->t2;
+    const int n = h->n, pp = h->sine_pitch;
+    launch_named(h, "repitch", [&] { launch_k(h->st, k_repitch, dim3(std::min(n, 1024), h->batch), 256, 0, src, dst, n, pp, n); });
+    op_dst_all(h, h->t2, xdev ? x : h->hout, s * s);
+  } else {
+    op_dst_all(h, h->kx, xdev ? x : h->hout, s);
+  }
   if (!xdev) FDE_CUDA(cudaMemcpyAsync(x, h->hout, h->vec_elems() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   const fde_status ws = worst_status(h, st, true);
   if (!h->no_graph && !persist1d) h->launches += (long long)read_loops(h) * h->g_pcg_nodes;

@@ -47,6 +47,7 @@ struct LineArgs {
   double2* zscr;          // variable Toeplitz: global scratch for the forward spectrum (L per line pair)
   int probe;              // phase-probe slot (FDE_PROBES builds only)
   int persist;            // sine-domain 1D body (MODE 5): loop inside the kernel until the RHS finishes
+  int pitch;              // sine-domain kernels: row pitch of the internal 2D vectors (0 = n)
   KryFuse kf;             // fused PCG vector work (krylov_kernels.cuh); kf.mode = 0: none
 };
 
@@ -74,6 +75,24 @@ __device__ __forceinline__ Line line_of(int l, int b, int n, int N) {
   L.stride = COL ? n : 1;
   L.fbase = COL ? l : l * n;
   return L;
+}
+
+// the same for the sine-domain kernels' internal 2D vectors, whose rows have
+// pitch p (= n+1, even: 16-byte aligned rows and column pairs); 1D: p = n
+template <bool COL>
+__device__ __forceinline__ Line line_of_pitch(int l, int b, int n, int pitch, bool two_d) {
+  Line L;
+  const long long per_rhs = two_d ? (long long)n * pitch : (long long)pitch;
+  L.base = (long long)b * per_rhs + (COL ? l : (long long)l * pitch);
+  L.stride = COL ? pitch : 1;
+  L.fbase = COL ? l : l * n;
+  return L;
+}
+
+// 16-byte asynchronous global -> shared copy
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
 }
 
 // 8-byte asynchronous global -> shared copy (LDGSTS): the copy proceeds while

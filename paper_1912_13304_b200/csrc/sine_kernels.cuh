@@ -96,7 +96,13 @@ k_sineop_lines(LineArgs a) {
   const int l0 = 2 * g, l1 = 2 * g + 1;
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
   const int n = m - 1;
-  const Line A0 = line_of<COL>(v0 ? l0 : 0, blockIdx.y, n, a.N), A1 = line_of<COL>(v1 ? l1 : 0, blockIdx.y, n, a.N);
+  const bool two_d = a.N != n;
+  const int pitch = a.pitch ? a.pitch : n;
+  const Line A0 = line_of_pitch<COL>(v0 ? l0 : 0, blockIdx.y, n, pitch, two_d);
+  const Line A1 = line_of_pitch<COL>(v1 ? l1 : 0, blockIdx.y, n, pitch, two_d);
+  // column pairs of an even pitch are adjacent, 16-byte aligned doubles:
+  // (line 0, line 1) of a row move as one double2
+  const bool vec2 = COL && v1 && (pitch & 1) == 0;
 
   for (;;) {  // one loop body; MODE 5 with a.persist repeats it until the RHS finishes
   // 1. stage the operator input in shared memory (natural order)
@@ -122,8 +128,14 @@ k_sineop_lines(LineArgs a) {
       else { src[0] = a.x; }
 #pragma unroll
       for (int c = 0; c < NV; ++c) {
-        g0v[c][i] = (ok && v0) ? src[c][o0] : 0.0;
-        g1v[c][i] = (ok && v1) ? src[c][o1] : 0.0;
+        if (vec2) {
+          const double2 pr = ok ? *reinterpret_cast<const double2*>(src[c] + o0) : make_double2(0.0, 0.0);
+          g0v[c][i] = pr.x;
+          g1v[c][i] = pr.y;
+        } else {
+          g0v[c][i] = (ok && v0) ? src[c][o0] : 0.0;
+          g1v[c][i] = (ok && v1) ? src[c][o1] : 0.0;
+        }
       }
       if (MODE != 1) {
         f0v[i] = (ok && v0) ? symbol_at<COL>(a, l0, e) : 1.0;
@@ -201,8 +213,12 @@ k_sineop_lines(LineArgs a) {
     for (int i = 0; i < RD; ++i) {
       const int e = RD * t + i - 1;
       if (e >= 0 && e < n) {
-        if (v0) cp_async8(&smW[GD::swz(e)].x, a.yin + A0.base + (long long)e * A0.stride);
-        if (v1) cp_async8(&smW[GD::swz(e)].y, a.yin + A1.base + (long long)e * A1.stride);
+        if (vec2) {
+          cp_async16(&smW[GD::swz(e)], a.yin + A0.base + (long long)e * A0.stride);
+        } else {
+          if (v0) cp_async8(&smW[GD::swz(e)].x, a.yin + A0.base + (long long)e * A0.stride);
+          if (v1) cp_async8(&smW[GD::swz(e)].y, a.yin + A1.base + (long long)e * A1.stride);
+        }
       }
     }
   }
@@ -290,6 +306,15 @@ k_sineop_lines(LineArgs a) {
     for (int i = 0; i < RD; ++i) {
       const int e = RD * t + i - 1;
       if (e < 0) continue;
+      if (vec2 && FDE_SINE_YIN_ASYNC) {  // both columns of the pair as one double2
+        const long long o = A0.base + (long long)e * A0.stride;
+        const double2 pv = *reinterpret_cast<const double2*>(a.kf.p + o);
+        const double2 yv = a.yin ? smW[GD::swz(e)] : make_double2(0.0, 0.0);
+        const double2 qv = make_double2(fma(a.nu, pv.x, g0[i] + yv.x), fma(a.nu, pv.y, g1[i] + yv.y));
+        *reinterpret_cast<double2*>(a.y + o) = qv;
+        acc[0] = fma(pv.x, qv.x, fma(pv.y, qv.y, acc[0]));
+        continue;
+      }
       if (v0) {
         const long long o = A0.base + (long long)e * A0.stride;
         const double pv = a.kf.p[o];
@@ -379,7 +404,7 @@ k_sineop_lines(LineArgs a) {
     for (int j = blockIdx.x; j < n; j += gridDim.x) {                             \
       const double fy = Fy[j];                                                    \
       for (int i = threadIdx.x; i < n; i += blockDim.x) {                         \
-        const size_t e = (size_t)j * n + i;                                       \
+        const size_t e = (size_t)j * pitch + i;                                   \
         const double F = Fx[i] + fy;                                              \
         BODY                                                                      \
       }                                                                           \
@@ -398,11 +423,11 @@ k_sineop_lines(LineArgs a) {
 // its XR_U elements of the row before any arithmetic (loads in flight).
 constexpr int XR_U = 4;
 __global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, const double* __restrict__ Fx,
-                                                 const double* __restrict__ Fy) {
+                                                 const double* __restrict__ Fy, int pitch) {
   FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
   if (!k.st[rhs].cyc_active) return;
-  const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * n : (size_t)n);
+  const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * pitch : (size_t)n);
   const double al = k.st[rhs].alpha;
   double* __restrict__ xr = k.x + o;
   double* __restrict__ rr = k.r + o;
@@ -412,7 +437,7 @@ __global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, con
   const int rows = dims == 2 ? n : 1;
   for (int j = blockIdx.x; j < rows; j += gridDim.x) {
     const double fy = dims == 2 ? Fy[j] : 0.0;
-    const size_t rb = (size_t)j * n;
+    const size_t rb = (size_t)j * (dims == 2 ? pitch : n);
     for (int i0 = threadIdx.x; i0 < n; i0 += XR_U * blockDim.x) {
       double qv[XR_U], rv[XR_U], pv[XR_U], xv[XR_U], fv[XR_U];
 #pragma unroll
@@ -443,10 +468,10 @@ __global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, con
 
 // sine-domain PCG start: x̂ = 0, p̂ = 0, ‖b̂‖, ρ = Σ r̂²/F, β = 0 (r̂ = b̂ already formed)
 __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, const double* __restrict__ Fx,
-                                                   const double* __restrict__ Fy) {
+                                                   const double* __restrict__ Fy, int pitch) {
   FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
-  const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * n : (size_t)n);
+  const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * pitch : (size_t)n);
   double acc[3] = {0.0, 0.0, 0.0};
   FDE_SINE_LOOP({
     const double rv = k.r[o + e];
@@ -460,6 +485,16 @@ __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, c
   KryFuse ki = k;
   ki.mode = KM_INIT;
   kry_reduce_finalize(ki, acc);
+}
+
+// copy 2D arrays between row pitches (user layout pitch n <-> internal pitch)
+__global__ void k_repitch(const double* __restrict__ src, double* __restrict__ dst, int n, int pitch_src, int pitch_dst) {
+  FDE_PDL_ENTRY();
+  const int rhs = blockIdx.y;
+  const double* s = src + (size_t)rhs * n * pitch_src;
+  double* d = dst + (size_t)rhs * n * pitch_dst;
+  for (int j = blockIdx.x; j < n; j += gridDim.x)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) d[(size_t)j * pitch_dst + i] = s[(size_t)j * pitch_src + i];
 }
 
 }  // namespace fde
