@@ -17,6 +17,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/fde.h"
@@ -779,6 +780,18 @@ void build(fde_handle h, const fde_desc* d) {
                       const std::vector<double>& fm) {
     std::vector<std::complex<double>> lam = lambda(order);
     const double invL = 1.0 / L;
+    // multiplier tables are read in the DIF output layout: lane t holds the
+    // 2^k consecutive bit-reversed positions s = (t << k) | q. Stored
+    // lane-major (entry q·P + t, P = L >> k) so one warp-wide load of a fixed
+    // q is contiguous instead of one 2^k-element stride per lane.
+    auto lane_major = [&](const auto& v, int k, size_t off) {
+      std::remove_cv_t<std::remove_reference_t<decltype(v)>> o(v);
+      const int P = L >> k;
+      for (int t = 0; t < P; ++t)
+        for (int q = 0; q < (1 << k); ++q) o[off + (size_t)q * P + t] = v[off + ((size_t)t << k) + q];
+      return o;
+    };
+    const int ks = sine_kd(h->K - 1) + 1;  // sine kernels: the Toeplitz FFT's points per thread
     if (!var) {
       // μ = (d+ + d-) Re λ + i (d+ - d-) Im λ (constant coefficients)
       std::vector<double2> mv(L);
@@ -787,7 +800,7 @@ void build(fde_handle h, const fde_desc* d) {
         // C(ν + λ) restricted to the leading n×n block is νI + (the Toeplitz part)
         mv[s] = make_double2((shift + wgt * (cpl + cmi) * l.real()) * invL, wgt * (cpl - cmi) * l.imag() * invL);
       }
-      mu = h->upload(mv);
+      mu = h->upload(lane_major(mv, KR, 0));
       // sine domain: D T D / (2m) = S T S with D = sqrt(2m) S; no ν (applied once, per element)
       std::vector<double2> ms(L);
       const double s2m = 1.0 / (2.0 * m);
@@ -795,7 +808,7 @@ void build(fde_handle h, const fde_desc* d) {
         const std::complex<double> l = lam[bitrev_host(s, h->K)];
         ms[s] = make_double2(wgt * (cpl + cmi) * l.real() * invL * s2m, wgt * (cpl - cmi) * l.imag() * invL * s2m);
       }
-      mus = h->upload(ms);
+      mus = h->upload(lane_major(ms, ks, 0));
     } else {
       std::vector<double> s1(L), s2(L);
       std::vector<double2> mv(2 * L);  // two-pass fallback multipliers
@@ -806,9 +819,9 @@ void build(fde_handle h, const fde_desc* d) {
         mv[s] = make_double2(s1[s], 0.0);
         mv[L + s] = make_double2(0.0, s2[s]);
       }
-      lS = h->upload(s1);
-      lK = h->upload(s2);
-      mu = h->upload(mv);
+      lS = h->upload(lane_major(s1, KR, 0));
+      lK = h->upload(lane_major(s2, KR, 0));
+      mu = h->upload(lane_major(lane_major(mv, KR, 0), KR, L));
       std::vector<double> p(N), q(N);
       for (int i = 0; i < N; ++i) { p[i] = wgt * (fp[i] + fm[i]); q[i] = wgt * (fp[i] - fm[i]); }
       cPf = h->upload(p);

@@ -30,9 +30,9 @@ struct LineArgs {
   const double2* twp;     // per-pass twiddle tables of the length-L FFT (fft_engine.cuh)
   const double2* twpm;    // per-pass twiddle tables of the length-m FFT (dst_kernels.cuh)
   const double* sinm;     // sin(πj/m), j = 0..m-1 (dst_kernels.cuh)
-  const double2* mu;      // const Toeplitz: complex multiplier, bit-reversed order, 1/L folded
-  const double* lamS;     // variable Toeplitz: Re λ / L (bit-reversed order)
-  const double* lamK;     // variable Toeplitz: Im λ / L (bit-reversed order)
+  const double2* mu;      // const Toeplitz: complex multiplier, bit-reversed order (lane-major), 1/L folded
+  const double* lamS;     // variable Toeplitz: Re λ / L (bit-reversed order, lane-major: entry q·P + t)
+  const double* lamK;     // variable Toeplitz: Im λ / L (bit-reversed order, lane-major)
   const double* cP;       // variable: field d+ + d- (length N) — multiplies the symmetric part
   const double* cM;       // variable: field d+ - d- (length N) — multiplies the skew part
   const double* omul;     // const-chain kernel: optional per-element multiplier of the chain output
@@ -197,7 +197,7 @@ k_toeplitz_lines(LineArgs a) {
   double2 u[G::R / 2];
   if (!VAR) {
 #pragma unroll
-    for (int q = 0; q < G::R; ++q) v[q] = c_mul(v[q], a.mu[(t << k) | q]);
+    for (int q = 0; q < G::R; ++q) v[q] = c_mul(v[q], a.mu[q * G::P + t]);  // lane-major table
     dit_chain<G, +1>(v, sm, t, tws);
   } else {
     // the forward spectrum is parked in a global (L2-resident) scratch for the
@@ -207,9 +207,8 @@ k_toeplitz_lines(LineArgs a) {
     double2* zs = a.zscr + ((size_t)(blockIdx.y * gridDim.x) * FPC + g) * G::L;
 #pragma unroll
     for (int q = 0; q < G::R; ++q) {
-      const int s = (t << k) | q;
       zs[q * G::P + t] = v[q];
-      v[q] = c_scale(v[q], a.lamS[s]);
+      v[q] = c_scale(v[q], a.lamS[q * G::P + t]);  // lane-major table
     }
     dit_chain<G, +1>(v, sm, t, tws);
 #pragma unroll
@@ -217,9 +216,8 @@ k_toeplitz_lines(LineArgs a) {
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < G::R; ++q) {
-      const int s = (t << k) | q;
       const double2 z = zs[q * G::P + t];
-      const double lk = a.lamK[s];
+      const double lk = a.lamK[q * G::P + t];
       v[q] = make_double2(-lk * z.y, lk * z.x);  // i·Im λ ⊙ Z
     }
     dit_chain<G, +1>(v, sm, t, tws);

@@ -254,7 +254,7 @@ k_sineop_lines(LineArgs a) {
   // 4. T̃ via the circulant embedding (μ_s carries d or e, 1/L and 1/(2m))
   dif_chain<GT, -1, true>(v, sm, t, twt);
 #pragma unroll
-  for (int q = 0; q < GT::R; ++q) v[q] = c_mul(v[q], a.mu[(t << GT::k) | q]);
+  for (int q = 0; q < GT::R; ++q) v[q] = c_mul(v[q], a.mu[q * GT::P + t]);  // lane-major table
   dit_chain<GT, +1>(v, sm, t, twt);
   __syncthreads();
 #pragma unroll
