@@ -258,6 +258,7 @@ struct fde_handle_s {
   double* sinm = nullptr;
   double2 *mu_x = nullptr, *mu_y = nullptr;
   double2 *mus_x = nullptr, *mus_y = nullptr;  // sine-domain μ_s (constant directions; sine_kernels.cuh)
+  double2* mus_xn = nullptr;  // μ_s of the x direction with ν folded in (2D row pass: q̂ = ν p̂ + ... there)
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
   double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
   double *invF = nullptr, *Fx = nullptr, *Fy = nullptr;
@@ -286,6 +287,8 @@ struct fde_handle_s {
   int g_maxit = -1;
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
+  bool sine_xr_rows = false;        // FDE_SINE_XR=rows: the per-row vector step instead of the flat one
+  bool sine_pqs = true;             // p̂·q̂ of the 2D sine body from the spectra (FDE_SINE_PQ=direct: elementwise)
   bool no_graph = false;            // env FDE_GRAPH=0: host-driven loop (for profilers)
   int sine_pitch = 0;               // row pitch of the sine-domain PCG's internal 2D vectors (n+1)
   bool sine_legacy = true;          // 3-kernel sine-domain body; env FDE_SINE_BODY=2: the recurrence body (A/B)
@@ -376,7 +379,7 @@ void launch_dstm_k(fde_handle h, const LineArgs& a) {
 }
 
 template <int KM, bool COL, int MODE>
-void launch_sineop_k(fde_handle h, const LineArgs& a0) {
+int launch_sineop_k(fde_handle h, const LineArgs& a0) {
   using C = LaunchCfgS<KM, COL, MODE>;
   LineArgs a = a0;
   a.twpm = h->twps_d;
@@ -392,6 +395,7 @@ void launch_sineop_k(fde_handle h, const LineArgs& a0) {
   const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
   launch_named(h, (MODE == 0 || MODE == 3) ? "sine_op_rows" : ((MODE == 1 || MODE == 4) ? "sine_op_cols" : "sine_op_1d"),
                [&] { launch_k(h->st, kern, grid, C::THREADS, C::SMEM, a); });
+  return (int)grid.x;
 }
 
 #define FDE_SWITCH_K(K, CALL)                                           \
@@ -777,7 +781,7 @@ void build(fde_handle h, const fde_desc* d) {
   auto make_dir = [&](double order, bool var, double cpl, double cmi, double wgt, double shift, double2*& mu, double2*& mus,
                       double*& lS,
                       double*& lK, double*& cPf, double*& cMf, const std::vector<double>& fp,
-                      const std::vector<double>& fm) {
+                      const std::vector<double>& fm, double2** musn) {
     std::vector<std::complex<double>> lam = lambda(order);
     const double invL = 1.0 / L;
     // multiplier tables are read in the DIF output layout: lane t holds the
@@ -809,6 +813,11 @@ void build(fde_handle h, const fde_desc* d) {
         ms[s] = make_double2(wgt * (cpl + cmi) * l.real() * invL * s2m, wgt * (cpl - cmi) * l.imag() * invL * s2m);
       }
       mus = h->upload(lane_major(ms, ks, 0));
+      if (musn) {
+        // D (T̃/(2m) + ν/(2m) I) D = S T̃ S + ν I: ν/(2m) on every eigenvalue (1/L folded)
+        for (int s = 0; s < L; ++s) ms[s].x += shift * s2m * invL;
+        *musn = h->upload(lane_major(ms, ks, 0));
+      }
     } else {
       std::vector<double> s1(L), s2(L);
       std::vector<double2> mv(2 * L);  // two-pass fallback multipliers
@@ -829,8 +838,8 @@ void build(fde_handle h, const fde_desc* d) {
     }
   };
   if (!h->dense) {
-    make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, d->nu, h->mu_x, h->mus_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm);
-    if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, 0.0, h->mu_y, h->mus_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em);
+    make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, d->nu, h->mu_x, h->mus_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm, &h->mus_xn);
+    if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, 0.0, h->mu_y, h->mus_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em, nullptr);
   }
 
   // preconditioner tables
@@ -934,6 +943,10 @@ void build(fde_handle h, const fde_desc* d) {
     h->no_graph = g && std::strcmp(g, "0") == 0;
     const char* sb = std::getenv("FDE_SINE_BODY");
     h->sine_legacy = !(sb && std::strcmp(sb, "2") == 0);
+    const char* pq = std::getenv("FDE_SINE_PQ");
+    h->sine_pqs = !(pq && std::strcmp(pq, "direct") == 0);
+    const char* xe = std::getenv("FDE_SINE_XR");
+    h->sine_xr_rows = xe && std::strcmp(xe, "rows") == 0;
     const char* s1 = std::getenv("FDE_SINE1D");
     h->sine1d_graph = s1 && std::strcmp(s1, "graph") == 0;
     const char* pd = std::getenv("FDE_PDL");
@@ -1242,7 +1255,13 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     a.y = h->wx;
     a.kf = kf;
     a.kf.mode = KM_PUPD | KM_GATE;
-    FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 0>(h, a)));
+    if (h->sine_pqs) {  // p̂·q̂ from the spectra of both passes, ν folded into the row multiplier
+      a.mu = h->mus_xn;
+      a.kf.mode |= KM_PQS | KM_PQX;
+    }
+    int rows_grid = 0;
+    FDE_SWITCH_K(h->K, (rows_grid = launch_sineop_k<KK - 1, false, 0>(h, a)));
+    if (rows_grid > KPMAX / 2) throw FdeFail{FDE_ERR_UNSUPPORTED, "row pass grid exceeds the partial region"};
     LineArgs b = base_args(h);
     b.nlines = h->n;
     b.x = h->kp;
@@ -1252,6 +1271,11 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     b.nu = h->d.nu;
     b.kf = kf;
     b.kf.mode = KM_PQ | KM_GATE;
+    if (h->sine_pqs) {
+      b.nu = 0.0;
+      b.kf.mode |= KM_PQS;
+      b.kf.xpart = rows_grid;
+    }
     FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, true, 1>(h, b)));
   } else {
     a.nlines = 1;
@@ -1273,7 +1297,13 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
   }();
   const int gx = dims == 2 ? std::min(n, xr_grid) : 64;
   const int pitch = h->sine_pitch;
-  launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr, dim3(gx, h->batch), 256, 0, kv, n, dims, Fx, Fy, pitch); });
+  if (dims == 2 && (pitch & (pitch - 1)) == 0 && !h->sine_xr_rows) {
+    int lgp = 0;
+    while ((1 << lgp) < pitch) ++lgp;
+    launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr2, dim3(xr_grid, h->batch), 256, 0, kv, n, lgp, Fx, Fy); });
+  } else {
+    launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr, dim3(gx, h->batch), 256, 0, kv, n, dims, Fx, Fy, pitch); });
+  }
 }
 
 fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, int maxit, fde_stats* st) {

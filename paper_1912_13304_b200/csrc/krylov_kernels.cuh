@@ -534,7 +534,12 @@ __global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const doub
 //            (= k) and convergence for k >= 1; ρ_k = r_k·z_k -> β_k = ρ_k/ρ_{k-1}
 // Partials: kpart[(rhs*3 + slot)*KPMAX + blockIdx.x]; the last CTA of each RHS
 // (ticket) sums them in fixed order (deterministic) and updates SolveState.
-enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16, KM_INIT = 32, KM_SROW = 64 };
+//   KM_PQS   sine-domain line pass: this pass's share of p·q from the spectrum,
+//            p·(S T̃ S p) = Σ_k Re μ_k |Z_k|² (Parseval; sine_kernels.cuh)
+//   KM_PQX   store the CTA's slot-0 partial in the extra region
+//            kpart[(rhs*3)*KPMAX + KPMAX/2 + blockIdx.x] and stop (no ticket);
+//            a later KM_PQ pass with KryFuse::xpart = that grid size adds them
+enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16, KM_INIT = 32, KM_SROW = 64, KM_PQS = 128, KM_PQX = 256 };
 constexpr int KPMAX = 4096;   // CTAs per RHS of one line kernel
 
 struct KryFuse {
@@ -548,6 +553,7 @@ struct KryFuse {
   double* part;
   double rtol;
   int maxit;
+  int xpart;   // extra slot-0 partials (KM_PQX of an earlier pass) summed by the finalising CTA
 };
 
 __device__ __forceinline__ void finish_rhs(Counters* c, SolveState& s) {
@@ -593,6 +599,7 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
     sl[1] += __ldcg(pr + KPMAX + b);
     sl[2] += __ldcg(pr + 2 * KPMAX + b);
   }
+  for (int b = threadIdx.x; b < k.xpart; b += blockDim.x) sl[0] += __ldcg(pr + KPMAX / 2 + b);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const double v = warp_sum(sl[i]);

@@ -251,10 +251,26 @@ k_sineop_lines(LineArgs a) {
   for (int q = GT::R / 2; q < GT::R; ++q) v[q] = make_double2(0.0, 0.0);
   __syncthreads();
 
+  const bool pqs_on = (a.kf.mode & KM_PQS) != 0;
+  __shared__ double s_pq[32];
+  double pq_part = 0.0;
   // 4. T̃ via the circulant embedding (μ_s carries d or e, 1/L and 1/(2m))
   dif_chain<GT, -1, true>(v, sm, t, twt);
 #pragma unroll
-  for (int q = 0; q < GT::R; ++q) v[q] = c_mul(v[q], a.mu[q * GT::P + t]);  // lane-major table
+  for (int q = 0; q < GT::R; ++q) {
+    const double2 mq = a.mu[q * GT::P + t];  // lane-major table
+    // KM_PQS: p·(this pass's operator p) = Σ_k Re μ_k |Z_k|² over the packed
+    // pair (Parseval for the unnormalised forward/inverse pair and the real
+    // circulant; the zero padding makes the full-length sum the n-element dot).
+    // Re(conj Z · μZ) = Re μ |Z|², taken from the product (no extra live values)
+    const double2 z = v[q];
+    v[q] = c_mul(z, mq);
+    if (pqs_on) pq_part = fma(z.x, v[q].x, fma(z.y, v[q].y, pq_part));
+  }
+  if (pqs_on) {  // park the warp's share in shared memory (nothing stays live through DST #2)
+    pq_part = warp_sum(pq_part);
+    if ((threadIdx.x & 31) == 0) s_pq[threadIdx.x >> 5] = pq_part;
+  }
   dit_chain<GT, +1>(v, sm, t, twt);
   __syncthreads();
 #pragma unroll
@@ -302,10 +318,17 @@ k_sineop_lines(LineArgs a) {
   } else if (MODE == 1) {
     // columns: this lane owns rows e = RD t + i - 1 of its two columns
     if (FDE_SINE_YIN_ASYNC && a.yin) cp_async_wait_all();
+    const bool pqs = (a.kf.mode & KM_PQS) != 0;
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
       const int e = RD * t + i - 1;
       if (e < 0) continue;
+      if (pqs && vec2 && FDE_SINE_YIN_ASYNC) {  // q̂ = yin + op: p̂·q̂ came from the spectrum, ν is in the row pass
+        const long long o = A0.base + (long long)e * A0.stride;
+        const double2 yv = a.yin ? smW[GD::swz(e)] : make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(a.y + o) = make_double2(g0[i] + yv.x, g1[i] + yv.y);
+        continue;
+      }
       if (vec2 && FDE_SINE_YIN_ASYNC) {  // both columns of the pair as one double2
         const long long o = A0.base + (long long)e * A0.stride;
         const double2 pv = *reinterpret_cast<const double2*>(a.kf.p + o);
@@ -321,7 +344,7 @@ k_sineop_lines(LineArgs a) {
         const double yv = a.yin ? (FDE_SINE_YIN_ASYNC ? smW[GD::swz(e)].x : a.yin[o]) : 0.0;
         const double qv = fma(a.nu, pv, g0[i] + yv);
         a.y[o] = qv;
-        acc[0] = fma(pv, qv, acc[0]);
+        if (!pqs) acc[0] = fma(pv, qv, acc[0]);
       }
       if (v1) {
         const long long o = A1.base + (long long)e * A1.stride;
@@ -329,7 +352,7 @@ k_sineop_lines(LineArgs a) {
         const double yv = a.yin ? (FDE_SINE_YIN_ASYNC ? smW[GD::swz(e)].y : a.yin[o]) : 0.0;
         const double qv = fma(a.nu, pv, g1[i] + yv);
         a.y[o] = qv;
-        acc[0] = fma(pv, qv, acc[0]);
+        if (!pqs) acc[0] = fma(pv, qv, acc[0]);
       }
     }
   } else {
@@ -377,6 +400,7 @@ k_sineop_lines(LineArgs a) {
       }
     }
   }
+  if ((MODE == 0 || MODE == 1) && pqs_on) acc[0] += (threadIdx.x & 31) == 0 ? s_pq[threadIdx.x >> 5] : 0.0;
   if (MODE == 5) {  // α_k = ρ_k / (p̂·q̂) inside the CTA
     acc[1] = acc[2] = 0.0;
     block_reduce3(acc, scr);
@@ -385,6 +409,9 @@ k_sineop_lines(LineArgs a) {
       if (!(acc[0] > 0.0)) { s.status = isfinite(acc[0]) ? ST_NOT_SPD : ST_NONFINITE; finish_rhs(a.kf.ctr, s); }
       else s.alpha = s.rho / acc[0];
     }
+  } else if (MODE == 0 && (a.kf.mode & KM_PQX)) {  // the row pass's share of p̂·q̂, finalised by the column pass
+    block_reduce3(acc, scr);
+    if (threadIdx.x == 0) a.kf.part[(size_t)blockIdx.y * 3 * KPMAX + KPMAX / 2 + blockIdx.x] = acc[0];
   } else if (MODE == 1 || MODE == 2 || MODE == 4) {
     kry_reduce_finalize(a.kf, acc);
   } else if (MODE == 3) {
@@ -466,6 +493,59 @@ __global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, con
   kry_reduce_finalize(k, acc);
 }
 
+// 2D vector step over the internal layout (n rows of pitch 2^lgp >= n+1) as a
+// flat array of 16-byte pairs: no per-row loop, every thread issues the loads
+// of its XR2_U pairs before any arithmetic. The padding entries i >= n of
+// every row are zero in r̂, q̂, p̂, x̂ (k_sine_init) and stay zero here.
+#ifndef FDE_XR2_U
+#define FDE_XR2_U 2
+#endif
+constexpr int XR2_U = FDE_XR2_U;
+__global__ void __launch_bounds__(256) k_sine_xr2(KryFuse k, int n, int lgp, const double* __restrict__ Fx,
+                                                  const double* __restrict__ Fy) {
+  FDE_PDL_ENTRY();
+  const int rhs = blockIdx.y;
+  if (!k.st[rhs].cyc_active) return;
+  const int pitch = 1 << lgp;
+  const size_t o = (size_t)rhs * ((size_t)n << lgp);
+  const int npairs = (n << lgp) >> 1;
+  const double al = k.st[rhs].alpha;
+  double2* __restrict__ xr = reinterpret_cast<double2*>(k.x + o);
+  double2* __restrict__ rr = reinterpret_cast<double2*>(k.r + o);
+  const double2* __restrict__ pr = reinterpret_cast<const double2*>(k.p + o);
+  const double2* __restrict__ qr = reinterpret_cast<const double2*>(k.q + o);
+  const int T = gridDim.x * blockDim.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < npairs; c0 += XR2_U * T) {
+    double2 qv[XR2_U], rv[XR2_U], pv[XR2_U], xv[XR2_U], fv[XR2_U];
+#pragma unroll
+    for (int u = 0; u < XR2_U; ++u) {
+      const int c = c0 + u * T;
+      const bool ok = c < npairs;
+      const double2 z = make_double2(0.0, 0.0);
+      qv[u] = ok ? qr[c] : z;
+      rv[u] = ok ? rr[c] : z;
+      pv[u] = ok ? pr[c] : z;
+      xv[u] = ok ? xr[c] : z;
+      const int e = 2 * c, j = e >> lgp, i = e & (pitch - 1);
+      const double fy = ok ? Fy[j] : 0.0;
+      fv[u] = make_double2(ok && i < n ? Fx[i] + fy : 1.0, ok && i + 1 < n ? Fx[i + 1] + fy : 1.0);
+    }
+#pragma unroll
+    for (int u = 0; u < XR2_U; ++u) {
+      const int c = c0 + u * T;
+      const double2 r = make_double2(fma(-al, qv[u].x, rv[u].x), fma(-al, qv[u].y, rv[u].y));
+      if (c < npairs) {
+        rr[c] = r;
+        xr[c] = make_double2(fma(al, pv[u].x, xv[u].x), fma(al, pv[u].y, xv[u].y));
+      }
+      acc[1] = fma(r.x, r.x, fma(r.y, r.y, acc[1]));
+      acc[2] = fma(r.x * r.x, fast_rcp(fv[u].x), fma(r.y * r.y, fast_rcp(fv[u].y), acc[2]));
+    }
+  }
+  kry_reduce_finalize(k, acc);
+}
+
 // sine-domain PCG start: x̂ = 0, p̂ = 0, ‖b̂‖, ρ = Σ r̂²/F, β = 0 (r̂ = b̂ already formed)
 __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, const double* __restrict__ Fx,
                                                    const double* __restrict__ Fy, int pitch) {
@@ -481,6 +561,16 @@ __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, c
     acc[1] = fma(rv, rv, acc[1]);
     acc[2] = fma(rv * rv, fast_rcp(F), acc[2]);
   })
+  if (dims == 2 && pitch > n && threadIdx.x == 0) {  // zero padding (k_sine_xr2 relies on it)
+    for (int j = blockIdx.x; j < n; j += gridDim.x)
+      for (int i = n; i < pitch; ++i) {
+        const size_t e = o + (size_t)j * pitch + i;
+        k.r[e] = 0.0;
+        k.x[e] = 0.0;
+        k.p[e] = 0.0;
+        k.q[e] = 0.0;
+      }
+  }
   // reuse the fused finalisation: slot 1 -> ‖b̂‖, slot 2 -> ρ (mode bits select the init path)
   KryFuse ki = k;
   ki.mode = KM_INIT;

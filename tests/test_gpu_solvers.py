@@ -149,13 +149,15 @@ def _solve_with_env(torch, p, env):
 @pytest.mark.parametrize("cfg,n,batch", [(1, 127, 2), (3, 63, 1), (5, 255, 3), (3, 511, 1)])
 def test_pcg_sine_domain_and_standard_paths_agree_with_oracle(torch_cuda, cfg, n, batch):
     """Constant coefficients + τ: fde_pcg runs PCG in the sine basis (DESIGN.md
-    §5.4; FDE_SINE_BODY=2 selects its recurrence body); FDE_PCG=standard forces
-    the standard-domain fused iteration. All must match the oracle's PCG
-    (iterations ±1, solution 1e-9)."""
+    §5.4; FDE_SINE_BODY=2 selects its recurrence body, FDE_SINE_PQ=direct the
+    elementwise p̂·q̂ instead of the spectral one, FDE_SINE_XR=rows the per-row
+    vector step); FDE_PCG=standard forces the standard-domain fused iteration.
+    All must match the oracle's PCG (iterations ±1, solution 1e-9)."""
     p = W.config(cfg, n=n, batch=batch)
     s = oracle_system(p)
     ref = oracle_solve(p, s, "pcg")
-    for env in ({}, {"FDE_SINE_BODY": "2"}, {"FDE_PCG": "standard"}, {"FDE_SINE1D": "graph"}):
+    for env in ({}, {"FDE_SINE_BODY": "2"}, {"FDE_PCG": "standard"}, {"FDE_SINE1D": "graph"},
+                {"FDE_SINE_PQ": "direct"}, {"FDE_SINE_XR": "rows"}):
         stats, x = _solve_with_env(torch_cuda, p, env)
         for b in range(batch):
             xo, it_o, conv_o, _ = ref[b]
