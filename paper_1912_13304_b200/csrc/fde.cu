@@ -236,6 +236,21 @@ struct LaunchCfgS {
   static constexpr int SMEM = FPC * SPG + SCR;
 };
 
+// concurrent 2D body (k_sineop_rc): both roles use the row pass's group count
+#ifndef FDE_RC_FPC
+#define FDE_RC_FPC 1
+#endif
+template <int KM>
+struct LaunchCfgRC {
+  using R = LaunchCfgS<KM, false, 6>;
+  static constexpr int FPC = R::FPC * FDE_RC_FPC, P = R::P, THREADS = FPC * P;
+  static constexpr int SCRC0 = (FPC * (GroupScan<true, P, FPC>::NSEG + 1) * 2) * 8;
+  static constexpr int SCRC = SCRC0 > 96 * 8 ? SCRC0 : 96 * 8;
+  static constexpr int SCRR0 = (FPC * (GroupScan<false, P, FPC>::NSEG + 1) * 2) * 8;
+  static constexpr int SCR = SCRC > SCRR0 ? SCRC : (SCRR0 > 96 * 8 ? SCRR0 : 96 * 8);
+  static constexpr int SMEM = FPC * R::SPG + SCR;
+};
+
 }  // namespace
 
 // ======================================================================== handle
@@ -267,6 +282,7 @@ struct fde_handle_s {
   double cx = 1.0, cy = 1.0;
   // workspace
   double *wx = nullptr, *t1 = nullptr, *t2 = nullptr, *t3 = nullptr;
+  double* wy = nullptr;   // w_c of the concurrent sine body (internal pitch layout)
   double *hin = nullptr, *hout = nullptr;  // staging for host pointers
   // Krylov
   SolveState* sst = nullptr;
@@ -288,6 +304,7 @@ struct fde_handle_s {
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
   bool sine_xr_rows = false;        // FDE_SINE_XR=rows: the per-row vector step instead of the flat one
+  bool sine_rc = true;              // 2D sine body as one concurrent row+column launch (else two passes)
   bool sine_pqs = true;             // p̂·q̂ of the 2D sine body from the spectra (FDE_SINE_PQ=direct: elementwise)
   bool no_graph = false;            // env FDE_GRAPH=0: host-driven loop (for profilers)
   int sine_pitch = 0;               // row pitch of the sine-domain PCG's internal 2D vectors (n+1)
@@ -396,6 +413,28 @@ int launch_sineop_k(fde_handle h, const LineArgs& a0) {
   launch_named(h, (MODE == 0 || MODE == 3) ? "sine_op_rows" : ((MODE == 1 || MODE == 4) ? "sine_op_cols" : "sine_op_1d"),
                [&] { launch_k(h->st, kern, grid, C::THREADS, C::SMEM, a); });
   return (int)grid.x;
+}
+
+template <int KM>
+void launch_sineop_rc_k(fde_handle h, const LineArgs& ar0, const LineArgs& ac0) {
+  using C = LaunchCfgRC<KM>;
+  LineArgs ar = ar0, ac = ac0;
+  for (LineArgs* a : {&ar, &ac}) {
+    a->twpm = h->twps_d;
+    a->twp = h->twps_t;
+    a->pitch = h->sine_pitch;
+  }
+  auto kern = k_sineop_rc<KM, C::FPC>;
+  static bool attr = false;
+  if (!attr) {
+    FDE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  const int gr = ((ar.nlines + 1) / 2 + C::FPC - 1) / C::FPC;
+  const int gc = ((ac.nlines + 1) / 2 + C::FPC - 1) / C::FPC;
+  if (gr + gc > KPMAX) throw FdeFail{FDE_ERR_UNSUPPORTED, "concurrent sine body grid exceeds the partial slots"};
+  const dim3 grid(gr + gc, h->batch);
+  launch_named(h, "sine_op_rc", [&] { launch_k(h->st, kern, grid, C::THREADS, C::SMEM, ar, ac, gc); });
 }
 
 #define FDE_SWITCH_K(K, CALL)                                           \
@@ -928,6 +967,7 @@ void build(fde_handle h, const fde_desc* d) {
   const size_t ve = std::max(h->vec_elems(), (size_t)h->batch * (h->dims == 2 ? (size_t)n * m : (size_t)n));
   if (h->var_x || h->var_y) h->zscr = h->dalloc<double2>((size_t)h->batch * (m / 2 + 64) * L);
   h->wx = h->dalloc<double>(ve);
+  h->wy = h->dalloc<double>(ve);
   h->t1 = h->dalloc<double>(ve);
   h->t2 = h->dalloc<double>(ve);
   h->t3 = h->dalloc<double>(ve);
@@ -945,6 +985,10 @@ void build(fde_handle h, const fde_desc* d) {
     h->sine_legacy = !(sb && std::strcmp(sb, "2") == 0);
     const char* pq = std::getenv("FDE_SINE_PQ");
     h->sine_pqs = !(pq && std::strcmp(pq, "direct") == 0);
+    // concurrent body where it measured faster on the B200 (one RHS, n <= 2047;
+    // DESIGN.md §5.4); FDE_SINE_RC=1 / 0 forces it on / off
+    const char* rc = std::getenv("FDE_SINE_RC");
+    h->sine_rc = rc ? std::strcmp(rc, "0") != 0 : (h->batch == 1 && n <= 2047);
     const char* xe = std::getenv("FDE_SINE_XR");
     h->sine_xr_rows = xe && std::strcmp(xe, "rows") == 0;
     const char* s1 = std::getenv("FDE_SINE1D");
@@ -1213,6 +1257,14 @@ void op_dst_all(fde_handle h, const double* x, double* y, double oscale) {
   FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, true, false>(h, b)));
 }
 
+int xr_grid() {  // CTAs of the sine-domain vector step (FDE_XR_GRID)
+  static const int g = [] {
+    const char* e = std::getenv("FDE_XR_GRID");
+    return e ? std::atoi(e) : 592;
+  }();
+  return g;
+}
+
 void sine_iteration(fde_handle h, double rtol, int maxit) {
   KryFuse kf = make_kf(h, rtol, maxit);
   LineArgs a = base_args(h);
@@ -1247,6 +1299,30 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
       a.kf.mode = KM_GATE;
       FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 5>(h, a)));
     }
+    return;
+  }
+  if (h->dims == 2 && h->sine_rc) {
+    // concurrent body: rows + columns in one launch, then the vector step
+    a.nlines = h->n;
+    a.x = h->kr;
+    a.y = h->wx;
+    a.mu = h->mus_xn;
+    a.kf = kf;
+    a.kf.mode = KM_PQ | KM_PQS | KM_GATE;
+    LineArgs c = a;
+    c.y = h->wy;
+    c.mu = h->mus_y;
+    FDE_SWITCH_K(h->K, (launch_sineop_rc_k<KK - 1>(h, a, c)));
+    KryFuse kv = kf;
+    kv.mode = KM_XR | KM_RZ | KM_GATE;
+    const double* Fx = h->Fx;
+    const double* Fy = h->Fy;
+    const double *wr = h->wx, *wc = h->wy;
+    const int n = h->n, pitch = h->sine_pitch;
+    int lgp = 0;
+    while ((1 << lgp) < pitch) ++lgp;
+    if ((1 << lgp) != pitch) throw FdeFail{FDE_ERR_UNSUPPORTED, "sine pitch is not a power of two"};
+    launch_named(h, "sine_xr_rc", [&] { launch_k(h->st, k_sine_xr3, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc); });
     return;
   }
   if (h->dims == 2) {
@@ -1291,16 +1367,12 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
   const double* Fx = h->Fx;
   const double* Fy = h->dims == 2 ? h->Fy : nullptr;
   const int n = h->n, dims = h->dims;
-  static const int xr_grid = [] {
-    const char* e = std::getenv("FDE_XR_GRID");
-    return e ? std::atoi(e) : 592;
-  }();
-  const int gx = dims == 2 ? std::min(n, xr_grid) : 64;
+  const int gx = dims == 2 ? std::min(n, xr_grid()) : 64;
   const int pitch = h->sine_pitch;
   if (dims == 2 && (pitch & (pitch - 1)) == 0 && !h->sine_xr_rows) {
     int lgp = 0;
     while ((1 << lgp) < pitch) ++lgp;
-    launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr2, dim3(xr_grid, h->batch), 256, 0, kv, n, lgp, Fx, Fy); });
+    launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr2, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy); });
   } else {
     launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr, dim3(gx, h->batch), 256, 0, kv, n, dims, Fx, Fy, pitch); });
   }

@@ -75,10 +75,14 @@ __device__ __forceinline__ double symbol_at(const LineArgs& a, int l, int e) {
 // MODE 1: 2D column pass: y = q̂ = ν p̂ + yin + (S T̃_β S) p̂ along columns, partial p̂·q̂
 // MODE 2: 1D:            p̂ = r̂/F + β p̂, y = q̂ = ν p̂ + (S T̃ S) p̂, partial p̂·q̂
 // a.x = r̂ (MODE 0/2) or p̂ (MODE 1); a.kf.p = p̂; a.mu = the sine-domain μ_s.
+// MODE 6/7: the concurrent body (k_sineop_rc): row (6) and column (7) passes
+// of ONE launch, independent of each other: both form p̂ = r̂/F + β p̂_old on
+// the fly (not written back), apply their direction's operator and write it
+// (6: w_r = ν p̂ + (S T̃_α S) p̂ rows, ν in μ; 7: w_c = (S T̃_β S) p̂ columns);
+// p̂·q̂ = p̂·w_r + p̂·w_c from the spectra (KM_PQS), α by the launch's last CTA.
+// k_sine_xr3 then writes p̂ and forms q̂ = w_r + w_c for the vector step.
 template <int KM, bool COL, int FPC, int MODE>
-__global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), min_blocks_for(FPC * (1 << (KM - sine_kd(KM)))))
-k_sineop_lines(LineArgs a) {
-  FDE_PDL_ENTRY();
+__device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
   using GD = FftGeom<KM, sine_kd(KM)>;           // DST: length-m FFT, 2^KD points per thread
   using GT = FftGeom<KM + 1, sine_kd(KM) + 1>;   // Toeplitz: length-2m FFT, 2^(KD+1) points per thread
   static_assert(GD::P == GT::P, "one thread layout for both transforms");
@@ -92,7 +96,7 @@ k_sineop_lines(LineArgs a) {
   double2* smW = smem_all + (size_t)FPC * GT::SM_STRIDE + (size_t)f * GD::SM_STRIDE;
   double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * (GT::SM_STRIDE + ((MODE == 1 || MODE == 4) ? GD::SM_STRIDE : 0)));
   const TwSrc twd{nullptr, a.twpm}, twt{nullptr, a.twp};
-  const int g = blockIdx.x * FPC + f;
+  const int g = bx * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
   const int n = m - 1;
@@ -107,14 +111,14 @@ k_sineop_lines(LineArgs a) {
   for (;;) {  // one loop body; MODE 5 with a.persist repeats it until the RHS finishes
   // 1. stage the operator input in shared memory (natural order)
   SolveState* const sst = a.kf.st + blockIdx.y;
-  const double beta = (MODE == 0 || MODE == 2) ? sst->betac : 0.0;
+  const double beta = (MODE == 0 || MODE == 2 || MODE == 6 || MODE == 7) ? sst->betac : 0.0;
   const double alpha = (MODE == 3 || MODE == 5) ? sst->alpha : 0.0;
   double acc[3] = {0.0, 0.0, 0.0};
   {
     // phase 1: every global load of this thread's RD elements (no stores in
     // between, so they are all in flight together); phase 2: arithmetic,
     // write-backs and the shared-memory staging
-    constexpr int NV = (MODE == 3 || MODE == 5) ? 4 : ((MODE == 0 || MODE == 2) ? 2 : 1);
+    constexpr int NV = (MODE == 3 || MODE == 5) ? 4 : ((MODE == 0 || MODE == 2 || MODE >= 6) ? 2 : 1);
     double g0v[NV][RD], g1v[NV][RD], f0v[RD], f1v[RD];
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
@@ -123,7 +127,7 @@ k_sineop_lines(LineArgs a) {
       const long long o0 = A0.base + (long long)(ok ? e : 0) * A0.stride, o1 = A1.base + (long long)(ok ? e : 0) * A1.stride;
       const double* src[4];
       if (MODE == 3 || MODE == 5) { src[0] = a.kf.r; src[1] = a.kf.q; src[2] = a.kf.p; src[3] = a.kf.x; }
-      else if (MODE == 0 || MODE == 2) { src[0] = a.x; src[1] = a.kf.p; }
+      else if (MODE == 0 || MODE == 2 || MODE >= 6) { src[0] = a.x; src[1] = a.kf.p; }
       else if (MODE == 4) { src[0] = a.kf.r; }
       else { src[0] = a.x; }
 #pragma unroll
@@ -153,6 +157,9 @@ k_sineop_lines(LineArgs a) {
         p1 = fma(beta, g1v[1][i], g1v[0][i] * fast_rcp(f1v[i]));
         if (v0) a.kf.p[o0] = p0;
         if (v1) a.kf.p[o1] = p1;
+      } else if (MODE >= 6) {  // p̂ = ẑ + β p̂_old, kept on chip (k_sine_xr3 writes it)
+        p0 = fma(beta, g0v[1][i], g0v[0][i] * fast_rcp(f0v[i]));
+        p1 = fma(beta, g1v[1][i], g1v[0][i] * fast_rcp(f1v[i]));
       } else if (MODE == 3 || MODE == 5) {  // r̂ -= α q̂, x̂ += α p̂, ẑ = r̂/F
         const double r0 = fma(-alpha, g0v[1][i], g0v[0][i]), r1 = fma(-alpha, g1v[1][i], g1v[0][i]);
         p0 = r0 * fast_rcp(f0v[i]);
@@ -315,6 +322,19 @@ k_sineop_lines(LineArgs a) {
         acc[0] = fma(pv, qv, acc[0]);
       }
     }
+  } else if (MODE == 7) {  // columns of the concurrent body: w_c = op (one double2 per pair and row)
+#pragma unroll
+    for (int i = 0; i < RD; ++i) {
+      const int e = RD * t + i - 1;
+      if (e < 0) continue;
+      const long long o0 = A0.base + (long long)e * A0.stride;
+      if (vec2) {
+        *reinterpret_cast<double2*>(a.y + o0) = make_double2(g0[i], g1[i]);
+      } else {
+        if (v0) a.y[o0] = g0[i];
+        if (v1) a.y[A1.base + (long long)e * A1.stride] = g1[i];
+      }
+    }
   } else if (MODE == 1) {
     // columns: this lane owns rows e = RD t + i - 1 of its two columns
     if (FDE_SINE_YIN_ASYNC && a.yin) cp_async_wait_all();
@@ -368,7 +388,7 @@ k_sineop_lines(LineArgs a) {
       if (e >= n) continue;
       const double2 o = sm[GD::swz(e)];
       const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
-      if (MODE == 0 || MODE == 3) {
+      if (MODE == 0 || MODE == 3 || MODE == 6) {
         if (v0) a.y[o0] = o.x;
         if (v1) a.y[o1] = o.y;
       } else if (MODE == 5) {  // 1D recurrence body: q̂ = ν ẑ + (S T̃ S) ẑ + β q̂, p̂ = ẑ + β p̂
@@ -400,7 +420,7 @@ k_sineop_lines(LineArgs a) {
       }
     }
   }
-  if ((MODE == 0 || MODE == 1) && pqs_on) acc[0] += (threadIdx.x & 31) == 0 ? s_pq[threadIdx.x >> 5] : 0.0;
+  if ((MODE == 0 || MODE == 1 || MODE >= 6) && pqs_on) acc[0] += (threadIdx.x & 31) == 0 ? s_pq[threadIdx.x >> 5] : 0.0;
   if (MODE == 5) {  // α_k = ρ_k / (p̂·q̂) inside the CTA
     acc[1] = acc[2] = 0.0;
     block_reduce3(acc, scr);
@@ -412,7 +432,7 @@ k_sineop_lines(LineArgs a) {
   } else if (MODE == 0 && (a.kf.mode & KM_PQX)) {  // the row pass's share of p̂·q̂, finalised by the column pass
     block_reduce3(acc, scr);
     if (threadIdx.x == 0) a.kf.part[(size_t)blockIdx.y * 3 * KPMAX + KPMAX / 2 + blockIdx.x] = acc[0];
-  } else if (MODE == 1 || MODE == 2 || MODE == 4) {
+  } else if (MODE == 1 || MODE == 2 || MODE == 4 || MODE >= 6) {
     kry_reduce_finalize(a.kf, acc);
   } else if (MODE == 3) {
     kry_reduce_finalize(a.kf, acc);
@@ -421,6 +441,36 @@ k_sineop_lines(LineArgs a) {
   if (MODE != 5 || !a.persist) break;
   __syncthreads();  // persistent 1D solve: the next body reuses sm and reads this body's writes
   }
+}
+
+template <int KM, bool COL, int FPC, int MODE>
+__global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), min_blocks_for(FPC * (1 << (KM - sine_kd(KM)))))
+k_sineop_lines(LineArgs a) {
+  FDE_PDL_ENTRY();
+  sineop_body<KM, COL, FPC, MODE>(a, blockIdx.x);
+}
+
+// the concurrent 2D body: CTAs [0, gc) run the column pass (MODE 7), the rest
+// the row pass (MODE 6) -- one launch, one ticket (α after both), and the work
+// units of both directions balance over the SMs together
+#ifndef FDE_RC_INTERLEAVE
+#define FDE_RC_INTERLEAVE 0
+#endif
+template <int KM, int FPC>
+__global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), min_blocks_for(FPC * (1 << (KM - sine_kd(KM)))))
+k_sineop_rc(LineArgs ar, LineArgs ac, int gc) {
+  FDE_PDL_ENTRY();
+  // the longer column units are dispatched first (lower blockIdx), the row
+  // units fill the tail (measured: 2% faster than rows first at n = 1023)
+  const int b = blockIdx.x;
+#if FDE_RC_INTERLEAVE
+  // interleaved: column and row units alternate in dispatch order (gr == gc)
+  if ((b & 1) == 0) sineop_body<KM, true, FPC, 7>(ac, b >> 1);
+  else sineop_body<KM, false, FPC, 6>(ar, b >> 1);
+#else
+  if (b < gc) sineop_body<KM, true, FPC, 7>(ac, b);
+  else sineop_body<KM, false, FPC, 6>(ar, b - gc);
+#endif
 }
 
 // F at (i, j) in the sine domain (1D: Fy == nullptr)
@@ -541,6 +591,65 @@ __global__ void __launch_bounds__(256) k_sine_xr2(KryFuse k, int n, int lgp, con
       }
       acc[1] = fma(r.x, r.x, fma(r.y, r.y, acc[1]));
       acc[2] = fma(r.x * r.x, fast_rcp(fv[u].x), fma(r.y * r.y, fast_rcp(fv[u].y), acc[2]));
+    }
+  }
+  kry_reduce_finalize(k, acc);
+}
+
+// vector step of the concurrent body (after k_sineop_rc): p̂ = r̂/F + β p̂_old
+// (written), q̂ = w_r + w_c, x̂ += α p̂, r̂ -= α q̂, partials ‖r̂‖², r̂·ẑ. Flat over
+// the internal layout like k_sine_xr2; padding entries (i >= n) of w_r, w_c are
+// never written, so they are masked here.
+__global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, const double* __restrict__ Fx,
+                                                  const double* __restrict__ Fy, const double* __restrict__ wr_,
+                                                  const double* __restrict__ wc_) {
+  FDE_PDL_ENTRY();
+  const int rhs = blockIdx.y;
+  if (!k.st[rhs].cyc_active) return;
+  const int pitch = 1 << lgp;
+  const size_t o = (size_t)rhs * ((size_t)n << lgp);
+  const int npairs = (n << lgp) >> 1;
+  const double al = k.st[rhs].alpha, be = k.st[rhs].betac;
+  double2* __restrict__ xr = reinterpret_cast<double2*>(k.x + o);
+  double2* __restrict__ rr = reinterpret_cast<double2*>(k.r + o);
+  double2* __restrict__ pr = reinterpret_cast<double2*>(k.p + o);
+  const double2* __restrict__ wr = reinterpret_cast<const double2*>(wr_ + o);
+  const double2* __restrict__ wc = reinterpret_cast<const double2*>(wc_ + o);
+  const int T = gridDim.x * blockDim.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < npairs; c0 += XR2_U * T) {
+    double2 rv[XR2_U], pv[XR2_U], xv[XR2_U], av[XR2_U], bv[XR2_U], fv[XR2_U];
+    bool okx[XR2_U], oky[XR2_U];
+#pragma unroll
+    for (int u = 0; u < XR2_U; ++u) {
+      const int c = c0 + u * T;
+      const bool ok = c < npairs;
+      const double2 z = make_double2(0.0, 0.0);
+      rv[u] = ok ? rr[c] : z;
+      pv[u] = ok ? pr[c] : z;
+      xv[u] = ok ? xr[c] : z;
+      av[u] = ok ? wr[c] : z;
+      bv[u] = ok ? wc[c] : z;
+      const int e = 2 * c, j = e >> lgp, i = e & (pitch - 1);
+      const double fy = ok ? Fy[j] : 0.0;
+      okx[u] = ok && i < n;
+      oky[u] = ok && i + 1 < n;
+      fv[u] = make_double2(okx[u] ? Fx[i] + fy : 1.0, oky[u] ? Fx[i + 1] + fy : 1.0);
+    }
+#pragma unroll
+    for (int u = 0; u < XR2_U; ++u) {
+      const int c = c0 + u * T;
+      const double2 iF = make_double2(fast_rcp(fv[u].x), fast_rcp(fv[u].y));
+      const double2 p = make_double2(fma(be, pv[u].x, rv[u].x * iF.x), fma(be, pv[u].y, rv[u].y * iF.y));
+      const double2 q = make_double2(okx[u] ? av[u].x + bv[u].x : 0.0, oky[u] ? av[u].y + bv[u].y : 0.0);
+      const double2 r = make_double2(fma(-al, q.x, rv[u].x), fma(-al, q.y, rv[u].y));
+      if (c < npairs) {
+        pr[c] = p;
+        rr[c] = r;
+        xr[c] = make_double2(fma(al, p.x, xv[u].x), fma(al, p.y, xv[u].y));
+      }
+      acc[1] = fma(r.x, r.x, fma(r.y, r.y, acc[1]));
+      acc[2] = fma(r.x * r.x, iF.x, fma(r.y * r.y, iF.y, acc[2]));
     }
   }
   kry_reduce_finalize(k, acc);

@@ -151,13 +151,14 @@ def test_pcg_sine_domain_and_standard_paths_agree_with_oracle(torch_cuda, cfg, n
     """Constant coefficients + τ: fde_pcg runs PCG in the sine basis (DESIGN.md
     §5.4; FDE_SINE_BODY=2 selects its recurrence body, FDE_SINE_PQ=direct the
     elementwise p̂·q̂ instead of the spectral one, FDE_SINE_XR=rows the per-row
-    vector step); FDE_PCG=standard forces the standard-domain fused iteration.
+    vector step, FDE_SINE_RC=0 the two-pass body instead of the concurrent one); FDE_PCG=standard forces the standard-domain fused iteration.
     All must match the oracle's PCG (iterations ±1, solution 1e-9)."""
     p = W.config(cfg, n=n, batch=batch)
     s = oracle_system(p)
     ref = oracle_solve(p, s, "pcg")
     for env in ({}, {"FDE_SINE_BODY": "2"}, {"FDE_PCG": "standard"}, {"FDE_SINE1D": "graph"},
-                {"FDE_SINE_PQ": "direct"}, {"FDE_SINE_XR": "rows"}):
+                {"FDE_SINE_RC": "0"}, {"FDE_SINE_RC": "1"}, {"FDE_SINE_RC": "0", "FDE_SINE_PQ": "direct"},
+                {"FDE_SINE_RC": "0", "FDE_SINE_XR": "rows"}):
         stats, x = _solve_with_env(torch_cuda, p, env)
         for b in range(batch):
             xo, it_o, conv_o, _ = ref[b]
@@ -180,11 +181,14 @@ def test_pcg_variable_coefficients_standard_path(torch_cuda):
     assert relerr(x[0], xo) <= 1e-9
 
 
-def test_batch_rhs_are_independent_and_deterministic(torch_cuda):
+@pytest.mark.parametrize("body", ["0", "1"])
+def test_batch_rhs_are_independent_and_deterministic(torch_cuda, monkeypatch, body):
     """Per-RHS grids and per-RHS fixed-order reductions: a batch-3 solve equals
     the three single-RHS solves bitwise, and repeating a solve is bitwise
-    identical (S:L420)."""
+    identical. The 2D sine-domain body is picked by (batch, n) by
+    default, so it is pinned here (FDE_SINE_RC) for both."""
     from paper_1912_13304_b200 import fde
+    monkeypatch.setenv("FDE_SINE_RC", body)
     for cfg, n, solver in ((5, 255, "pcg"), (4, 127, "gmres")):
         p = W.config(cfg, n=n, batch=3)
         _, _, x3, _ = gpu_solve(torch_cuda, p, solver)
@@ -222,7 +226,7 @@ def test_profile_abis_report_every_kernel(torch_cuda):
     assert all(us > 0 for _, us in unit)
     x = torch_cuda.zeros_like(b)
     live, stats = h.profile_solve(b, x, "pcg", 1e-10, 4)
-    assert [nm for nm, _ in live] == ["sine_op_rows", "sine_op_cols", "sine_xr"]
+    assert [nm for nm, _ in live] == ["sine_op_rc", "sine_xr_rc"]   # one RHS, n <= 2047: the concurrent body
     assert stats[0]["iters"] == 4
     h.close()
     p = W.config(4, n=127)

@@ -27,13 +27,24 @@ for _ in range(2):
     h.pcg(b, x, 1e-10, 2)
     torch.cuda.synchronize()
     fde.lib.fde_debug_probes(buf.ctypes.data, buf.nbytes)
-for s, nm in ((4, "sine_op_rows"), (5, "sine_op_cols")):
-    bb = buf[s].astype(np.int64)
-    used = bb[:, 0] > 0
-    bb = bb[used]
-    t0 = bb[:, 0].min()
-    rel = (bb - t0) / 1e3
-    print("%-14s CTAs %4d start spread %.2f us end %.2f us" % (nm, used.sum(), rel[:, 0].max(), rel[:, 5].max()))
-    for i in range(5):
-        d = rel[:, i + 1] - rel[:, i]
-        print("   phase %d->%d  median %.2f  max %.2f us" % (i, i + 1, np.median(d), d.max()))
+# every probed launch slot of the last iteration; a concurrent-body launch
+# (sine_op_rc) is split into its column CTAs [0, gc) and row CTAs [gc, ...)
+gc = (p.n + 1) // 2
+for s in range(8):
+    bb_all = buf[s].astype(np.int64)
+    used_all = bb_all[:, 0] > 0
+    if used_all.sum() == 0:
+        continue
+    t0 = bb_all[used_all, 0].min()
+    ranges = [("all", np.arange(2048))]
+    if used_all.sum() > gc:
+        ranges = [("cols", np.arange(gc)), ("rows", np.arange(gc, 2048))]
+    for nm, idx in ranges:
+        bb = bb_all[idx]
+        used = bb[:, 0] > 0
+        bb = bb[used]
+        rel = (bb - t0) / 1e3
+        print("slot %d %-5s CTAs %4d start spread %.2f us end %.2f us" % (s, nm, used.sum(), rel[:, 0].max(), rel[:, 5].max()))
+        for i in range(5):
+            d = rel[:, i + 1] - rel[:, i]
+            print("   phase %d->%d  median %.2f  max %.2f us" % (i, i + 1, np.median(d), d.max()))
