@@ -12,5 +12,5 @@ FDE_GRAPH=0 python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/
 FDE_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; echo "ncu1 rc=$?"
 FDE_GRAPH=0 python tools/unit_run.py --reps 1 --pcg > gpurun_out/plain2.log 2>&1 && \
-FDE_GRAPH=0 ncu --set full --clock-control none --import-source on -k regex:"k_sineop_lines|k_sine_xr" -s 6 -c 3 \
+FDE_GRAPH=0 ncu --set full --clock-control none --import-source on -k regex:"k_sineop|k_sine_xr" -s 6 -c 4 \
     -o gpurun_out/prof_iter python tools/unit_run.py --reps 1 --pcg > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"

@@ -90,6 +90,10 @@ def _short(name):
     if "k_sineop_lines" in n:
         mode = n.split("<")[1].split(">")[0].split(",")[3].strip()
         return {"0": "sine_op_rows", "1": "sine_op_cols", "2": "sine_op_1d"}[mode]
+    if "k_sineop_rc" in n:
+        return "sine_op_rc"
+    if "k_sine_xr3" in n:
+        return "sine_xr_rc"
     if "k_sine_xr" in n:
         return "sine_xr"
     return n
