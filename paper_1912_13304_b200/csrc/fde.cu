@@ -303,6 +303,7 @@ struct fde_handle_s {
   int g_maxit = -1;
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
+  bool sine_xr4 = true;             // 32-byte vector step of the concurrent body (FDE_XR4=0: 16-byte)
   bool sine_xr_rows = false;        // FDE_SINE_XR=rows: the per-row vector step instead of the flat one
   bool sine_rc = true;              // 2D sine body as one concurrent row+column launch (else two passes)
   bool sine_pqs = true;             // p̂·q̂ of the 2D sine body from the spectra (FDE_SINE_PQ=direct: elementwise)
@@ -989,6 +990,8 @@ void build(fde_handle h, const fde_desc* d) {
     // DESIGN.md §5.4); FDE_SINE_RC=1 / 0 forces it on / off
     const char* rc = std::getenv("FDE_SINE_RC");
     h->sine_rc = rc ? std::strcmp(rc, "0") != 0 : (h->batch == 1 && n <= 2047);
+    const char* x4 = std::getenv("FDE_XR4");
+    h->sine_xr4 = !(x4 && std::strcmp(x4, "0") == 0);
     const char* xe = std::getenv("FDE_SINE_XR");
     h->sine_xr_rows = xe && std::strcmp(xe, "rows") == 0;
     const char* s1 = std::getenv("FDE_SINE1D");
@@ -1322,7 +1325,10 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     int lgp = 0;
     while ((1 << lgp) < pitch) ++lgp;
     if ((1 << lgp) != pitch) throw FdeFail{FDE_ERR_UNSUPPORTED, "sine pitch is not a power of two"};
-    launch_named(h, "sine_xr_rc", [&] { launch_k(h->st, k_sine_xr3, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc); });
+    if (h->sine_xr4 && lgp >= 2)
+      launch_named(h, "sine_xr_rc", [&] { launch_k(h->st, k_sine_xr4, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc); });
+    else
+      launch_named(h, "sine_xr_rc", [&] { launch_k(h->st, k_sine_xr3, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc); });
     return;
   }
   if (h->dims == 2) {

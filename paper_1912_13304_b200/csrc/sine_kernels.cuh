@@ -29,6 +29,16 @@ __host__ __device__ constexpr int sine_kd(int KM) {
 #endif
 }
 
+// resident CTAs per SM the sine kernels' register budget is sized for
+// (FDE_SINE_MINB overrides: measured A/B of occupancy against spills)
+__host__ __device__ constexpr int sine_minb(int threads) {
+#ifdef FDE_SINE_MINB
+  return FDE_SINE_MINB;
+#else
+  return min_blocks_for(threads);
+#endif
+}
+
 // CTA-wide fixed-order sum of acc[0..2]; the result is valid in thread 0.
 // scr: >= 3*32 doubles of shared memory; ends with a barrier.
 __device__ __forceinline__ void block_reduce3(double (&acc)[3], double* scr) {
@@ -444,7 +454,7 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
 }
 
 template <int KM, bool COL, int FPC, int MODE>
-__global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), min_blocks_for(FPC * (1 << (KM - sine_kd(KM)))))
+__global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), sine_minb(FPC * (1 << (KM - sine_kd(KM)))))
 k_sineop_lines(LineArgs a) {
   FDE_PDL_ENTRY();
   sineop_body<KM, COL, FPC, MODE>(a, blockIdx.x);
@@ -457,7 +467,7 @@ k_sineop_lines(LineArgs a) {
 #define FDE_RC_INTERLEAVE 0
 #endif
 template <int KM, int FPC>
-__global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), min_blocks_for(FPC * (1 << (KM - sine_kd(KM)))))
+__global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), sine_minb(FPC * (1 << (KM - sine_kd(KM)))))
 k_sineop_rc(LineArgs ar, LineArgs ac, int gc) {
   FDE_PDL_ENTRY();
   // the longer column units are dispatched first (lower blockIdx), the row
@@ -650,6 +660,88 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, 
       }
       acc[1] = fma(r.x, r.x, fma(r.y, r.y, acc[1]));
       acc[2] = fma(r.x * r.x, iF.x, fma(r.y * r.y, iF.y, acc[2]));
+    }
+  }
+  kry_reduce_finalize(k, acc);
+}
+
+// 32-byte accesses (sm_100 LDG.E.256 / STG.E.256)
+struct alignas(32) dbl4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ dbl4 ld4(const double* p) {
+  dbl4 v;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4(double* p, const dbl4& v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+
+// k_sine_xr3 over 32-byte groups of 4 elements (pitch a multiple of 4)
+#ifndef FDE_XR4_U
+#define FDE_XR4_U 1
+#endif
+__global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, const double* __restrict__ Fx,
+                                                     const double* __restrict__ Fy, const double* __restrict__ wr_,
+                                                     const double* __restrict__ wc_) {
+  FDE_PDL_ENTRY();
+  constexpr int U = FDE_XR4_U;
+  const int rhs = blockIdx.y;
+  if (!k.st[rhs].cyc_active) return;
+  const int pitch = 1 << lgp;
+  const size_t o = (size_t)rhs * ((size_t)n << lgp);
+  const int nq = (n << lgp) >> 2;
+  const double al = k.st[rhs].alpha, be = k.st[rhs].betac;
+  double* __restrict__ xr = k.x + o;
+  double* __restrict__ rr = k.r + o;
+  double* __restrict__ pr = k.p + o;
+  const double* __restrict__ wr = wr_ + o;
+  const double* __restrict__ wc = wc_ + o;
+  const int T = gridDim.x * blockDim.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < nq; c0 += U * T) {
+    dbl4 rv[U], pv[U], xv[U], av[U], bv[U];
+    double fy[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * T;
+      const bool ok = c < nq;
+      const size_t e = (size_t)(ok ? c : 0) * 4;
+      rv[u] = ld4(rr + e);
+      pv[u] = ld4(pr + e);
+      xv[u] = ld4(xr + e);
+      av[u] = ld4(wr + e);
+      bv[u] = ld4(wc + e);
+      fy[u] = Fy[(int)(e >> lgp)];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * T;
+      const int e = 4 * c, i = e & (pitch - 1);
+      double* rp = &rv[u].x;
+      double* pp = &pv[u].x;
+      double* xp = &xv[u].x;
+      const double* ap = &av[u].x;
+      const double* bp = &bv[u].x;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const bool ok = i + s < n;
+        const double iF = fast_rcp(ok ? Fx[i + s] + fy[u] : 1.0);
+        const double pn = fma(be, pp[s], rp[s] * iF);
+        const double q = ok ? ap[s] + bp[s] : 0.0;
+        const double r = fma(-al, q, rp[s]);
+        pp[s] = pn;
+        xp[s] = fma(al, pn, xp[s]);
+        rp[s] = r;
+        acc[1] = fma(r, r, acc[1]);
+        acc[2] = fma(r * r, iF, acc[2]);
+      }
+      if (c < nq) {
+        st4(pr + (size_t)e, pv[u]);
+        st4(rr + (size_t)e, rv[u]);
+        st4(xr + (size_t)e, xv[u]);
+      }
     }
   }
   kry_reduce_finalize(k, acc);

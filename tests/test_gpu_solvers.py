@@ -157,7 +157,8 @@ def test_pcg_sine_domain_and_standard_paths_agree_with_oracle(torch_cuda, cfg, n
     s = oracle_system(p)
     ref = oracle_solve(p, s, "pcg")
     for env in ({}, {"FDE_SINE_BODY": "2"}, {"FDE_PCG": "standard"}, {"FDE_SINE1D": "graph"},
-                {"FDE_SINE_RC": "0"}, {"FDE_SINE_RC": "1"}, {"FDE_SINE_RC": "0", "FDE_SINE_PQ": "direct"},
+                {"FDE_SINE_RC": "0"}, {"FDE_SINE_RC": "1"}, {"FDE_SINE_RC": "1", "FDE_XR4": "0"},
+                {"FDE_SINE_RC": "0", "FDE_SINE_PQ": "direct"},
                 {"FDE_SINE_RC": "0", "FDE_SINE_XR": "rows"}):
         stats, x = _solve_with_env(torch_cuda, p, env)
         for b in range(batch):
