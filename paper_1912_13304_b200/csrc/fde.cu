@@ -303,6 +303,7 @@ struct fde_handle_s {
   int g_maxit = -1;
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
+  bool gm_ws = true;                // warp-split CGS kernels for j < 32 (FDE_GM_WS=0: one thread per element)
   bool sine_xr4 = true;             // 32-byte vector step of the concurrent body (FDE_XR4=0: 16-byte)
   bool sine_xr_rows = false;        // FDE_SINE_XR=rows: the per-row vector step instead of the flat one
   bool sine_rc = true;              // 2D sine body as one concurrent row+column launch (else two passes)
@@ -990,6 +991,8 @@ void build(fde_handle h, const fde_desc* d) {
     // DESIGN.md §5.4); FDE_SINE_RC=1 / 0 forces it on / off
     const char* rc = std::getenv("FDE_SINE_RC");
     h->sine_rc = rc ? std::strcmp(rc, "0") != 0 : (h->batch == 1 && n <= 2047);
+    const char* gw = std::getenv("FDE_GM_WS");
+    h->gm_ws = !(gw && std::strcmp(gw, "0") == 0);
     const char* x4 = std::getenv("FDE_XR4");
     h->sine_xr4 = !(x4 && std::strcmp(x4, "0") == 0);
     const char* xe = std::getenv("FDE_SINE_XR");
@@ -1504,12 +1507,23 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
       op_matvec(h, Vj, h->kq, gA);
       op_tau(h, h->kq, Vn, gA);
     }
-    launch_named(h, "gm_mdot", [&] { launch_k(h->st, k_gm_mdot, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
-    if (j < 32)
-      launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k_gm_upd_mdot32, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
-    else
-      launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k_gm_upd_mdot, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
-    launch_named(h, "gm_upd_norm", [&] { launch_k(h->st, k_gm_upd_norm, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+    if (j < 32 && h->gm_ws) {  // warp-split CGS passes (krylov_kernels.cuh)
+      auto cgs = [&](auto k0, auto k1, auto k2) {
+        launch_named(h, "gm_mdot", [&] { launch_k(h->st, k0, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+        launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k1, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+        launch_named(h, "gm_upd_norm", [&] { launch_k(h->st, k2, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+      };
+      if (j < 8) cgs(k_gm_cgs_ws<0, 1, 16>, k_gm_cgs_ws<1, 1, 16>, k_gm_cgs_ws<2, 1, 16>);
+      else if (j < 16) cgs(k_gm_cgs_ws<0, 2, 8>, k_gm_cgs_ws<1, 2, 8>, k_gm_cgs_ws<2, 2, 8>);
+      else cgs(k_gm_cgs_ws<0, 4, 4>, k_gm_cgs_ws<1, 4, 4>, k_gm_cgs_ws<2, 4, 4>);
+    } else {
+      launch_named(h, "gm_mdot", [&] { launch_k(h->st, k_gm_mdot, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+      if (j < 32)
+        launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k_gm_upd_mdot32, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+      else
+        launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k_gm_upd_mdot, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+      launch_named(h, "gm_upd_norm", [&] { launch_k(h->st, k_gm_upd_norm, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+    }
     if (j + 1 < restart) launch_named(h, "gm_scale", [&] { launch_k(h->st, k_gm_scale, VGRID, RED_THREADS, 0, va, Vn); });
   }
   // end of cycle: x += P⁻¹(V y) (right) or V y (left); restart residual

@@ -365,6 +365,48 @@ __global__ void __launch_bounds__(RED_THREADS) k_gm_upd_mdot32(VecArgs a, const 
   if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, a.gs[rb].h2);
 }
 
+// Arnoldi/Givens step of column j after the last CGS pass, given ‖w‖²
+// (thread 0 of the last block; SolveState, H, Givens rotations, g, stopping)
+__device__ __forceinline__ void arnoldi_step(VecArgs& a, int rb, int j, double nrm2) {
+  SolveState& s = a.st[rb];
+  GmresSmall& gs = a.gs[rb];
+  constexpr int LD = MAX_RESTART + 1;
+  double* Hc = gs.H + (size_t)j * LD;
+  for (int i = 0; i <= j; ++i) Hc[i] = gs.h[i] + gs.h2[i];
+  const double hn = sqrt(nrm2);
+  Hc[j + 1] = hn;
+  for (int i = 0; i < j; ++i) {
+    const double t = gs.cs[i] * Hc[i] + gs.sn[i] * Hc[i + 1];
+    Hc[i + 1] = -gs.sn[i] * Hc[i] + gs.cs[i] * Hc[i + 1];
+    Hc[i] = t;
+  }
+  const double den = hypot(Hc[j], Hc[j + 1]);
+  gs.cs[j] = Hc[j] / den;
+  gs.sn[j] = Hc[j + 1] / den;
+  Hc[j] = den;
+  Hc[j + 1] = 0.0;
+  gs.g[j + 1] = -gs.sn[j] * gs.g[j];
+  gs.g[j] = gs.cs[j] * gs.g[j];
+  s.iters += 1;
+  s.kused = j + 1;
+  s.rnorm = fabs(gs.g[j + 1]) / s.bnorm;
+  s.inv_h = 1.0 / hn;
+  bool stop = false;
+  if (!isfinite(hn) || !isfinite(den)) {
+    s.status = ST_NONFINITE;
+    stop = true;
+  } else if (fabs(gs.g[j + 1]) <= a.rtol * s.bnorm) {
+    s.converged = 1;
+    stop = true;
+  } else if (hn == 0.0) {
+    s.status = ST_BREAKDOWN;
+    stop = true;
+  } else if (s.iters >= a.maxit || j + 1 >= a.restart) {
+    stop = true;  // end of cycle (or of the budget)
+  }
+  if (stop && s.cyc_active) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
+}
+
 // CGS pass 2 update + norm + Arnoldi/Givens step (thread 0 of the last block)
 __global__ void k_gm_upd_norm(VecArgs a, const double* __restrict__ V, size_t vstride, double* w, int j) {
   FDE_PDL_ENTRY();
@@ -390,44 +432,126 @@ __global__ void k_gm_upd_norm(VecArgs a, const double* __restrict__ V, size_t vs
   if (last_block(&a.ctr->tickets[rb * 8])) {
     __shared__ double out[1];
     finalize(part, 1, out);
-    if (threadIdx.x == 0) {
-      SolveState& s = a.st[rb];
-      GmresSmall& gs = a.gs[rb];
-      constexpr int LD = MAX_RESTART + 1;
-      double* Hc = gs.H + (size_t)j * LD;
-      for (int i = 0; i <= j; ++i) Hc[i] = gs.h[i] + gs.h2[i];
-      const double hn = sqrt(out[0]);
-      Hc[j + 1] = hn;
-      for (int i = 0; i < j; ++i) {
-        const double t = gs.cs[i] * Hc[i] + gs.sn[i] * Hc[i + 1];
-        Hc[i + 1] = -gs.sn[i] * Hc[i] + gs.cs[i] * Hc[i + 1];
-        Hc[i] = t;
+    if (threadIdx.x == 0) arnoldi_step(a, rb, j, out[0]);
+  }
+}
+
+// Warp-split CGS passes (j < 32). The 8 warps of a block split the basis:
+// warp k holds V_i, i = k + 8s (s < 4), at the block's chunk of 128
+// elements (4 per lane, coalesced), so a thread keeps <= 16 V values in
+// registers instead of 32 (k_gm_upd_mdot32: 166 registers, one block per SM,
+// latency-bound). Per chunk, the cross-warp sum Σ_i h_i V_i(e) goes through
+// shared memory in fixed order (k = 0..7), then the dots of pass 2 reuse the
+// V values still in registers (V is read from memory once per pass).
+//   MODE 0: h = Vᵀ w
+//   MODE 1: w -= V h ; h2 = Vᵀ w
+//   MODE 2: w -= V h2 ; ‖w‖² -> Arnoldi/Givens step
+// NS = vector slots per warp (nv <= 8 NS), EPL = elements per lane per
+// chunk; NS·EPL = 16 keeps the registers fixed while small bases still keep
+// enough bytes in flight (the chunk grows as the basis shrinks).
+template <int MODE, int NS, int EPL>
+__global__ void __launch_bounds__(256) k_gm_cgs_ws(VecArgs a, const double* __restrict__ V, size_t vstride,
+                                                   double* __restrict__ w, int j) {
+  constexpr int WS_CHUNK = 32 * EPL;
+  FDE_PDL_ENTRY();
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  const int nv = j + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ double ws_w[WS_CHUNK];
+  __shared__ double ws_p[8][WS_CHUNK];
+  static_assert(WS_CHUNK <= 512, "one pass of the block covers the chunk");
+  __shared__ double hs[32];
+  if (MODE != 0)
+    for (int i = threadIdx.x; i < 32; i += blockDim.x)
+      hs[i] = i < nv ? __ldcg(MODE == 1 ? &a.gs[rb].h[i] : &a.gs[rb].h2[i]) : 0.0;
+  double acc[NS > 1 ? NS : 1];
+#pragma unroll
+  for (int sl = 0; sl < (NS > 1 ? NS : 1); ++sl) acc[sl] = 0.0;
+  double nrm = 0.0;
+  __syncthreads();
+  for (long long c0 = (long long)blockIdx.x * WS_CHUNK; c0 < N; c0 += (long long)gridDim.x * WS_CHUNK) {
+    double vv[NS][EPL];
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int i = wid + 8 * sl;
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) {
+        const long long e = c0 + lane + 32 * u;
+        vv[sl][u] = (i < nv && e < N) ? __ldg(V + (size_t)i * vstride + o + e) : 0.0;
       }
-      const double den = hypot(Hc[j], Hc[j + 1]);
-      gs.cs[j] = Hc[j] / den;
-      gs.sn[j] = Hc[j + 1] / den;
-      Hc[j] = den;
-      Hc[j + 1] = 0.0;
-      gs.g[j + 1] = -gs.sn[j] * gs.g[j];
-      gs.g[j] = gs.cs[j] * gs.g[j];
-      s.iters += 1;
-      s.kused = j + 1;
-      s.rnorm = fabs(gs.g[j + 1]) / s.bnorm;
-      s.inv_h = 1.0 / hn;
-      bool stop = false;
-      if (!isfinite(hn) || !isfinite(den)) {
-        s.status = ST_NONFINITE;
-        stop = true;
-      } else if (fabs(gs.g[j + 1]) <= a.rtol * s.bnorm) {
-        s.converged = 1;
-        stop = true;
-      } else if (hn == 0.0) {
-        s.status = ST_BREAKDOWN;
-        stop = true;
-      } else if (s.iters >= a.maxit || j + 1 >= a.restart) {
-        stop = true;  // end of cycle (or of the budget)
+    }
+    constexpr int TPT = (WS_CHUNK + 255) / 256;  // chunk elements per thread in the w phase
+    double wv[TPT];
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      const int t = threadIdx.x + 256 * q;
+      const long long ec = c0 + t;
+      wv[q] = (t < WS_CHUNK && ec < N) ? w[o + ec] : 0.0;
+    }
+    if (MODE == 0) {
+#pragma unroll
+      for (int q = 0; q < TPT; ++q)
+        if (threadIdx.x + 256 * q < WS_CHUNK) ws_w[threadIdx.x + 256 * q] = wv[q];
+      __syncthreads();
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl)
+#pragma unroll
+        for (int u = 0; u < EPL; ++u) acc[sl] = fma(vv[sl][u], ws_w[lane + 32 * u], acc[sl]);
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) {
+        double ps = 0.0;
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) ps = fma(hs[wid + 8 * sl], vv[sl][u], ps);
+        ws_p[wid][lane + 32 * u] = ps;
       }
-      if (stop && s.cyc_active) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < TPT; ++q) {
+        const int t = threadIdx.x + 256 * q;
+        if (t < WS_CHUNK) {
+          double sum = 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) sum += ws_p[k][t];
+          const double wn = wv[q] - sum;
+          const long long ec = c0 + t;
+          if (ec < N) w[o + ec] = wn;
+          if (MODE == 1) ws_w[t] = wn;
+          else nrm = fma(wn, wn, nrm);
+        }
+      }
+      if (MODE == 1) {
+        __syncthreads();
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl)
+#pragma unroll
+          for (int u = 0; u < EPL; ++u) acc[sl] = fma(vv[sl][u], ws_w[lane + 32 * u], acc[sl]);
+      }
+      __syncthreads();
+    }
+  }
+  double* part = a.part + (size_t)rb * (MAX_RESTART + 1) * RED_BLOCKS;
+  if (MODE != 2) {
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int i = wid + 8 * sl;
+      const double v = warp_sum(acc[sl]);
+      if (lane == 0 && i < nv) part[(size_t)i * RED_BLOCKS + blockIdx.x] = v;
+    }
+    if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, MODE == 0 ? a.gs[rb].h : a.gs[rb].h2);
+  } else {
+    __shared__ double red[32];
+    double n2[1] = {nrm};
+    block_sum<1>(n2, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = n2[0];
+    if (last_block(&a.ctr->tickets[rb * 8])) {
+      __shared__ double out[1];
+      finalize(part, 1, out);
+      if (threadIdx.x == 0) arnoldi_step(a, rb, j, out[0]);
     }
   }
 }

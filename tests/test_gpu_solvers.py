@@ -78,6 +78,23 @@ def test_solver_parity(torch_cuda, cfg, n, batch, solver, prec):
         assert np.linalg.norm(r) / np.linalg.norm(p.rhs[b]) <= 1e-9
 
 
+@pytest.mark.parametrize("ws", ["0", "1"])
+def test_gmres_cgs_kernel_variants(torch_cuda, monkeypatch, ws):
+    """Both CGS2 kernel families (FDE_GM_WS=1: warp-split passes, the default
+    for j < 32; 0: one thread per element) match the oracle's GMRES(30)."""
+    monkeypatch.setenv("FDE_GM_WS", ws)
+    for cfg, n, batch, prec in ((2, 255, 2, W.PREC_TAU_D), (4, 127, 1, W.PREC_TAU)):
+        p = W.config(cfg, n=n, batch=batch, prec=prec)
+        s = oracle_system(p)
+        st, stats, x, _ = gpu_solve(torch_cuda, p, "gmres")
+        ref = oracle_solve(p, s, "gmres")
+        for b in range(batch):
+            xo, it_o, conv_o, _ = ref[b]
+            assert stats[b]["converged"] and conv_o
+            assert abs(stats[b]["iters"] - it_o) <= 1, (ws, b, stats[b]["iters"], it_o)
+            assert relerr(x[b], xo) <= 1e-9, (ws, relerr(x[b], xo))
+
+
 def test_gmres_left_unrestarted_matches_oracle(torch_cuda):
     p = W.config(2, n=255, prec=W.PREC_TAU_D)
     s = oracle_system(p)
