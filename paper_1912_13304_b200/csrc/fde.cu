@@ -1496,8 +1496,7 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
   const int* gU = &h->ctr->unfinished;
   const size_t vs = h->vec_elems();
   double* V = h->V;
-  launch_named(h, "gm_scale", [&] { launch_k(h->st, k_gm_scale, VGRID, RED_THREADS, 0, va, V); });
-  for (int j = 0; j < restart; ++j) {
+  for (int j = 0; j < restart; ++j) {  // basis vectors stay unnormalised (GmresSmall::vsc)
     double* Vj = V + (size_t)j * vs;
     double* Vn = V + (size_t)(j + 1) * vs;
     if (!left) {
@@ -1524,7 +1523,6 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
         launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k_gm_upd_mdot, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
       launch_named(h, "gm_upd_norm", [&] { launch_k(h->st, k_gm_upd_norm, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
     }
-    if (j + 1 < restart) launch_named(h, "gm_scale", [&] { launch_k(h->st, k_gm_scale, VGRID, RED_THREADS, 0, va, Vn); });
   }
   // end of cycle: x += P⁻¹(V y) (right) or V y (left); restart residual
   launch_named(h, "gm_lincomb", [&] { launch_k(h->st, k_gm_lincomb, VGRID, RED_THREADS, 0, va, V, vs, h->kp); });

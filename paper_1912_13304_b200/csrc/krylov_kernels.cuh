@@ -30,7 +30,6 @@ struct SolveState {          // one per RHS, device resident
   double beta;               // GMRES: current cycle's ‖r‖; PCG: unused
   double rho, alpha, betac;  // PCG scalars
   double rnorm;              // last residual estimate
-  double inv_h;              // GMRES: 1/H[j+1,j] of the last step (normalisation)
   int iters;                 // matvecs (PCG) / Arnoldi steps (GMRES)
   int cyc_active;            // GMRES: still stepping in this cycle; PCG: still iterating
   int finished;              // solution final
@@ -47,6 +46,10 @@ struct GmresSmall {          // one per RHS
   double h[MAX_RESTART + 1];                   // CGS pass 1 coefficients
   double h2[MAX_RESTART + 1];                  // CGS pass 2 coefficients
   double y[MAX_RESTART];
+  // lazy normalisation: basis vectors are stored unnormalised, V_i = vsc[i]·(stored V_i)
+  // (so no separate scaling pass over the new vector; the factors enter the
+  // dot and update coefficients)
+  double vsc[MAX_RESTART + 1];
 };
 
 struct Counters {            // device counters
@@ -111,6 +114,15 @@ __device__ __forceinline__ void finalize(const double* part, int nvec, double* o
     if (lane == 0) out[i] = s;
   }
   __syncthreads();
+}
+
+// dots of stored vectors -> true h_i = vsc[i]·vsc[j]·(V_i·w)_stored (all threads of the finalising block)
+__device__ __forceinline__ void gm_true_dots(const GmresSmall& gs, double* hv, int nv, int j) {
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) hv[i] *= gs.vsc[i] * gs.vsc[j];
+}
+// update coefficient of stored V_i for the stored w: h_i·vsc[i]/vsc[j]
+__device__ __forceinline__ double gm_coef(const GmresSmall& gs, const double* hv, int i, int j) {
+  return __ldcg(&hv[i]) * (__ldcg(&gs.vsc[i]) / __ldcg(&gs.vsc[j]));
 }
 
 struct VecArgs {
@@ -201,7 +213,7 @@ __global__ void k_pcg_init2(VecArgs a, const double* __restrict__ r, const doubl
 }
 
 // ========================================================== GMRES (a4) ====
-// init: x = 0, r = b (right) ; ref = ‖r‖ ; V0 = r/‖r‖ (done by k_gm_scale)
+// init: x = 0, r = b (right) ; ref = ‖r‖ ; V0 = r stored unnormalised (vsc[0] = 1/‖r‖)
 // For left preconditioning the caller passes r = P⁻¹b as `src`.
 __global__ void k_gm_init(VecArgs a, const double* __restrict__ src, double* x, double* V0) {
   FDE_PDL_ENTRY();
@@ -231,9 +243,9 @@ __global__ void k_gm_init(VecArgs a, const double* __restrict__ src, double* x, 
       s.converged = 0;
       s.status = ST_OK;
       s.rnorm = 1.0;
-      s.inv_h = 1.0 / s.beta;
       GmresSmall& gs = a.gs[rb];
       gs.g[0] = s.beta;
+      gs.vsc[0] = 1.0 / s.beta;
       if (!(s.bnorm > 0.0)) {
         s.converged = (s.bnorm == 0.0);
         if (!(s.bnorm == 0.0)) s.status = ST_NONFINITE;
@@ -242,17 +254,6 @@ __global__ void k_gm_init(VecArgs a, const double* __restrict__ src, double* x, 
       }
     }
   }
-}
-
-// V_j *= inv_h (normalise the new basis vector in place)
-__global__ void k_gm_scale(VecArgs a, double* Vj) {
-  FDE_PDL_ENTRY();
-  if (a.ctr->active == 0) return;
-  const int rb = blockIdx.y, N = a.N;
-  if (!a.st[rb].cyc_active) return;
-  const double s = a.st[rb].inv_h;
-  const size_t o = (size_t)rb * N;
-  FDE_GRID_LOOP(e) Vj[o + e] *= s;
 }
 
 // Vectors of the basis: V + i*vstride + rb*N
@@ -289,7 +290,10 @@ __global__ void k_gm_mdot(VecArgs a, const double* __restrict__ V, size_t vstrid
     if (threadIdx.x == 0)
       for (int c = 0; c < MD_CH && i0 + c < nv; ++c) part[(size_t)(i0 + c) * RED_BLOCKS + blockIdx.x] = acc[c];
   }
-  if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, a.gs[rb].h);
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    finalize(part, nv, a.gs[rb].h);
+    gm_true_dots(a.gs[rb], a.gs[rb].h, nv, j);
+  }
 }
 
 // CGS pass 1 update + pass 2 dots: w -= V h ; h2_i = V_iᵀ w
@@ -301,7 +305,7 @@ __global__ void k_gm_upd_mdot(VecArgs a, const double* __restrict__ V, size_t vs
   const size_t o = (size_t)rb * N;
   const int nv = j + 1;
   __shared__ double hs[MAX_RESTART + 1];
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = __ldcg(&a.gs[rb].h[i]);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = gm_coef(a.gs[rb], a.gs[rb].h, i, j);
   __syncthreads();
   FDE_GRID_LOOP(e) {
     double wv = w[o + e];
@@ -317,7 +321,10 @@ __global__ void k_gm_upd_mdot(VecArgs a, const double* __restrict__ V, size_t vs
     if (threadIdx.x == 0)
       for (int c = 0; c < MD_CH && i0 + c < nv; ++c) part[(size_t)(i0 + c) * RED_BLOCKS + blockIdx.x] = acc[c];
   }
-  if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, a.gs[rb].h2);
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    finalize(part, nv, a.gs[rb].h2);
+    gm_true_dots(a.gs[rb], a.gs[rb].h2, nv, j);
+  }
 }
 
 // CGS pass 1 update + pass 2 dots in ONE pass over V (j < 32): per element,
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_gm_upd_mdot32(VecArgs a, const 
   const size_t o = (size_t)rb * N;
   const int nv = j + 1;
   __shared__ double hs[32];
-  for (int i = threadIdx.x; i < 32; i += blockDim.x) hs[i] = i < nv ? __ldcg(&a.gs[rb].h[i]) : 0.0;
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) hs[i] = i < nv ? gm_coef(a.gs[rb], a.gs[rb].h, i, j) : 0.0;
   __syncthreads();
   double acc[32];
 #pragma unroll
@@ -362,7 +369,10 @@ __global__ void __launch_bounds__(RED_THREADS) k_gm_upd_mdot32(VecArgs a, const 
     if (threadIdx.x == 0)
       for (int i = 0; i < MD_CH && 8 * c + i < nv; ++i) part[(size_t)(8 * c + i) * RED_BLOCKS + blockIdx.x] = ch[i];
   }
-  if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, a.gs[rb].h2);
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    finalize(part, nv, a.gs[rb].h2);
+    gm_true_dots(a.gs[rb], a.gs[rb].h2, nv, j);
+  }
 }
 
 // Arnoldi/Givens step of column j after the last CGS pass, given ‖w‖²
@@ -373,7 +383,9 @@ __device__ __forceinline__ void arnoldi_step(VecArgs& a, int rb, int j, double n
   constexpr int LD = MAX_RESTART + 1;
   double* Hc = gs.H + (size_t)j * LD;
   for (int i = 0; i <= j; ++i) Hc[i] = gs.h[i] + gs.h2[i];
-  const double hn = sqrt(nrm2);
+  const double ws = sqrt(nrm2);      // ‖stored w‖
+  const double hn = gs.vsc[j] * ws;  // ‖w‖ = H[j+1,j]
+  gs.vsc[j + 1] = 1.0 / ws;          // V_{j+1} = stored w / ‖stored w‖
   Hc[j + 1] = hn;
   for (int i = 0; i < j; ++i) {
     const double t = gs.cs[i] * Hc[i] + gs.sn[i] * Hc[i + 1];
@@ -390,7 +402,6 @@ __device__ __forceinline__ void arnoldi_step(VecArgs& a, int rb, int j, double n
   s.iters += 1;
   s.kused = j + 1;
   s.rnorm = fabs(gs.g[j + 1]) / s.bnorm;
-  s.inv_h = 1.0 / hn;
   bool stop = false;
   if (!isfinite(hn) || !isfinite(den)) {
     s.status = ST_NONFINITE;
@@ -416,7 +427,7 @@ __global__ void k_gm_upd_norm(VecArgs a, const double* __restrict__ V, size_t vs
   const size_t o = (size_t)rb * N;
   const int nv = j + 1;
   __shared__ double hs[MAX_RESTART + 1];
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = __ldcg(&a.gs[rb].h2[i]);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) hs[i] = gm_coef(a.gs[rb], a.gs[rb].h2, i, j);
   __syncthreads();
   double acc[1] = {0.0};
   FDE_GRID_LOOP(e) {
@@ -466,7 +477,7 @@ __global__ void __launch_bounds__(256) k_gm_cgs_ws(VecArgs a, const double* __re
   __shared__ double hs[32];
   if (MODE != 0)
     for (int i = threadIdx.x; i < 32; i += blockDim.x)
-      hs[i] = i < nv ? __ldcg(MODE == 1 ? &a.gs[rb].h[i] : &a.gs[rb].h2[i]) : 0.0;
+      hs[i] = i < nv ? gm_coef(a.gs[rb], MODE == 1 ? a.gs[rb].h : a.gs[rb].h2, i, j) : 0.0;
   double acc[NS > 1 ? NS : 1];
 #pragma unroll
   for (int sl = 0; sl < (NS > 1 ? NS : 1); ++sl) acc[sl] = 0.0;
@@ -542,7 +553,10 @@ __global__ void __launch_bounds__(256) k_gm_cgs_ws(VecArgs a, const double* __re
       const double v = warp_sum(acc[sl]);
       if (lane == 0 && i < nv) part[(size_t)i * RED_BLOCKS + blockIdx.x] = v;
     }
-    if (last_block(&a.ctr->tickets[rb * 8])) finalize(part, nv, MODE == 0 ? a.gs[rb].h : a.gs[rb].h2);
+    if (last_block(&a.ctr->tickets[rb * 8])) {
+      finalize(part, nv, MODE == 0 ? a.gs[rb].h : a.gs[rb].h2);
+      gm_true_dots(a.gs[rb], MODE == 0 ? a.gs[rb].h : a.gs[rb].h2, nv, j);
+    }
   } else {
     __shared__ double red[32];
     double n2[1] = {nrm};
@@ -563,7 +577,7 @@ __global__ void k_gm_lincomb(VecArgs a, const double* __restrict__ V, size_t vst
   const int rb = blockIdx.y, N = a.N;
   if (a.st[rb].finished) return;
   const size_t o = (size_t)rb * N;
-  __shared__ double ys[MAX_RESTART];
+  __shared__ double ys[MAX_RESTART], ys2[MAX_RESTART];
   const int ku = a.st[rb].kused;
   if (threadIdx.x == 0) {
     const GmresSmall& gs = a.gs[rb];
@@ -575,9 +589,11 @@ __global__ void k_gm_lincomb(VecArgs a, const double* __restrict__ V, size_t vst
     }
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < ku; i += blockDim.x) ys2[i] = ys[i] * a.gs[rb].vsc[i];  // stored V_i
+  __syncthreads();
   FDE_GRID_LOOP(e) {
     double acc = 0.0;
-    for (int i = 0; i < ku; ++i) acc = fma(ys[i], __ldg(V + (size_t)i * vstride + o + e), acc);
+    for (int i = 0; i < ku; ++i) acc = fma(ys2[i], __ldg(V + (size_t)i * vstride + o + e), acc);
     u[o + e] = acc;
   }
 }
@@ -635,7 +651,7 @@ __global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const doub
           s.status = ST_NONFINITE;
           mark_finished(a, s);
         } else {
-          s.inv_h = 1.0 / be;
+          a.gs[rb].vsc[0] = 1.0 / be;
           s.kused = 0;
           a.gs[rb].g[0] = be;
           if (!s.cyc_active) { s.cyc_active = 1; atomicAdd(&a.ctr->active, 1); }
