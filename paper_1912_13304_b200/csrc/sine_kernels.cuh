@@ -466,24 +466,16 @@ k_sineop_lines(LineArgs a) {
 // the concurrent 2D body: CTAs [0, gc) run the column pass (MODE 7), the rest
 // the row pass (MODE 6) -- one launch, one ticket (α after both), and the work
 // units of both directions balance over the SMs together
-#ifndef FDE_RC_INTERLEAVE
-#define FDE_RC_INTERLEAVE 0
-#endif
 template <int KM, int FPC>
 __global__ void __launch_bounds__(FPC * (1 << (KM - sine_kd(KM))), sine_minb(FPC * (1 << (KM - sine_kd(KM)))))
 k_sineop_rc(LineArgs ar, LineArgs ac, int gc) {
   FDE_PDL_ENTRY();
   // the longer column units are dispatched first (lower blockIdx), the row
-  // units fill the tail (measured: 2% faster than rows first at n = 1023)
+  // units fill the tail (measured at n = 1023: rows first -2%, rows and
+  // columns alternating -12%, one row unit per SM ahead of the columns ±0)
   const int b = blockIdx.x;
-#if FDE_RC_INTERLEAVE
-  // interleaved: column and row units alternate in dispatch order (gr == gc)
-  if ((b & 1) == 0) sineop_body<KM, true, FPC, 7>(ac, b >> 1);
-  else sineop_body<KM, false, FPC, 6>(ar, b >> 1);
-#else
   if (b < gc) sineop_body<KM, true, FPC, 7>(ac, b);
   else sineop_body<KM, false, FPC, 6>(ar, b - gc);
-#endif
 }
 
 // F at (i, j) in the sine domain (1D: Fy == nullptr)
