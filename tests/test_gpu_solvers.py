@@ -370,14 +370,19 @@ def test_orders_near_the_bounds(torch_cuda, alpha, beta):
     assert abs(stats[0]["iters"] - it_o) <= 1 and relerr(x[0], xo) <= 1e-9
 
 
-@pytest.mark.parametrize("cfg,n,batch,solver", [(5, 4095, 2, "pcg"), (5, 2047, 8, "pcg"), (2, 4095, 2, "gmres")])
-def test_full_size_solves_true_residual(torch_cuda, cfg, n, batch, solver):
+@pytest.mark.parametrize("cfg,n,batch,solver,rc", [(5, 4095, 2, "pcg", None), (5, 2047, 8, "pcg", None),
+                                                   (5, 2047, 1, "pcg", None), (5, 4095, 1, "pcg", "1"),
+                                                   (5, 1023, 1, "pcg", None), (2, 4095, 2, "gmres", None),
+                                                   (4, 1023, 1, "gmres", None)])
+def test_full_size_solves_true_residual(torch_cuda, monkeypatch, cfg, n, batch, solver, rc):
     """Largest sizes/batches the bench sweep runs: the dense oracle cannot
     solve them, so check what holds at any size — the true residual
     ‖b - A x‖/‖b‖ per RHS (A applied by fde_matvec, itself parity-tested at
     these sizes by sampled entries) meets the tolerance — and the iteration
     counts of all RHS agree with the single-RHS solve."""
     from paper_1912_13304_b200 import fde
+    if rc is not None:  # the concurrent sine body also at n = 4095 (by default only n <= 2047)
+        monkeypatch.setenv("FDE_SINE_RC", rc)
     p = W.config(cfg, n=n, batch=batch)
     h = fde.Fde.from_problem(p)
     b = torch_cuda.from_numpy(p.rhs.copy()).cuda()
