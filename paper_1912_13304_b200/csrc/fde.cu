@@ -1439,6 +1439,13 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   } else {
     FDE_CUDA(cudaGraphLaunch(h->g_pcg, h->st));
   }
+  if (h->dims == 2 && h->sine_rc) {  // the concurrent body's last x̂ += α p̂ (lagged by one step)
+    KryFuse kx = kf;
+    const int n = h->n;
+    int lgp = 0;
+    while ((1 << lgp) < h->sine_pitch) ++lgp;
+    launch_named(h, "sine_xfix", [&] { launch_k(h->st, k_sine_xfix, dim3(xr_grid(), h->batch), 256, 0, kx, n, lgp); });
+  }
   // x = (S⊗S) x̂ = (D⊗D) x̃ / (2m)^dims
   const double s = 1.0 / (2.0 * h->m);
   const bool xdev = is_device_ptr(x);

@@ -809,6 +809,7 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
     const double pq = tot[0];
     if (!(pq > 0.0)) {
       s.status = isfinite(pq) ? ST_NOT_SPD : ST_NONFINITE;
+      s.alpha = 0.0;  // no x update pending (the concurrent sine body lags x by one step)
       finish_rhs(k.ctr, s);
     } else {
       s.alpha = s.rho / pq;

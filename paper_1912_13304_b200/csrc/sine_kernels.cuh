@@ -122,13 +122,14 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
   // 1. stage the operator input in shared memory (natural order)
   SolveState* const sst = a.kf.st + blockIdx.y;
   const double beta = (MODE == 0 || MODE == 2 || MODE == 6 || MODE == 7) ? sst->betac : 0.0;
-  const double alpha = (MODE == 3 || MODE == 5) ? sst->alpha : 0.0;
+  // MODE 6 applies the lagged x̂ += α_{k-1} p̂_{k-1} (k_sine_xr3/4 leave x̂ alone)
+  const double alpha = (MODE == 3 || MODE == 5 || MODE == 6) ? sst->alpha : 0.0;
   double acc[3] = {0.0, 0.0, 0.0};
   {
     // phase 1: every global load of this thread's RD elements (no stores in
     // between, so they are all in flight together); phase 2: arithmetic,
     // write-backs and the shared-memory staging
-    constexpr int NV = (MODE == 3 || MODE == 5) ? 4 : ((MODE == 0 || MODE == 2 || MODE >= 6) ? 2 : 1);
+    constexpr int NV = (MODE == 3 || MODE == 5) ? 4 : (MODE == 6 ? 3 : ((MODE == 0 || MODE == 2 || MODE == 7) ? 2 : 1));
     double g0v[NV][RD], g1v[NV][RD], f0v[RD], f1v[RD];
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
@@ -137,7 +138,8 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
       const long long o0 = A0.base + (long long)(ok ? e : 0) * A0.stride, o1 = A1.base + (long long)(ok ? e : 0) * A1.stride;
       const double* src[4];
       if (MODE == 3 || MODE == 5) { src[0] = a.kf.r; src[1] = a.kf.q; src[2] = a.kf.p; src[3] = a.kf.x; }
-      else if (MODE == 0 || MODE == 2 || MODE >= 6) { src[0] = a.x; src[1] = a.kf.p; }
+      else if (MODE == 6) { src[0] = a.x; src[1] = a.kf.p; src[2] = a.kf.x; }
+      else if (MODE == 0 || MODE == 2 || MODE == 7) { src[0] = a.x; src[1] = a.kf.p; }
       else if (MODE == 4) { src[0] = a.kf.r; }
       else { src[0] = a.x; }
 #pragma unroll
@@ -173,6 +175,10 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
       } else if (MODE >= 6) {  // p̂ = ẑ + β p̂_old, kept on chip (k_sine_xr3 writes it)
         p0 = fma(beta, g0v[1][i], g0v[0][i] * fast_rcp(f0v[i]));
         p1 = fma(beta, g1v[1][i], g1v[0][i] * fast_rcp(f1v[i]));
+        if (MODE == 6) {  // lagged x̂ update of the previous iteration (rows: coalesced)
+          if (v0) a.kf.x[o0] = fma(alpha, g0v[1][i], g0v[NV - 1][i]);
+          if (v1) a.kf.x[o1] = fma(alpha, g1v[1][i], g1v[NV - 1][i]);
+        }
       } else if (MODE == 3 || MODE == 5) {  // r̂ -= α q̂, x̂ += α p̂, ẑ = r̂/F
         const double r0 = fma(-alpha, g0v[1][i], g0v[0][i]), r1 = fma(-alpha, g1v[1][i], g1v[0][i]);
         p0 = r0 * fast_rcp(f0v[i]);
@@ -602,7 +608,8 @@ __global__ void __launch_bounds__(256) k_sine_xr2(KryFuse k, int n, int lgp, con
 }
 
 // vector step of the concurrent body (after k_sineop_rc): p̂ = r̂/F + β p̂_old
-// (written), q̂ = w_r + w_c, x̂ += α p̂, r̂ -= α q̂, partials ‖r̂‖², r̂·ẑ. Flat over
+// (written), q̂ = w_r + w_c, r̂ -= α q̂, partials ‖r̂‖², r̂·ẑ. x̂ += α p̂ is
+// lagged: the next row pass applies it (k_sine_xfix after the last iteration). Flat over
 // the internal layout like k_sine_xr2; padding entries (i >= n) of w_r, w_c are
 // never written, so they are masked here.
 __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, const double* __restrict__ Fx,
@@ -615,7 +622,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, 
   const size_t o = (size_t)rhs * ((size_t)n << lgp);
   const int npairs = (n << lgp) >> 1;
   const double al = k.st[rhs].alpha, be = k.st[rhs].betac;
-  double2* __restrict__ xr = reinterpret_cast<double2*>(k.x + o);
   double2* __restrict__ rr = reinterpret_cast<double2*>(k.r + o);
   double2* __restrict__ pr = reinterpret_cast<double2*>(k.p + o);
   const double2* __restrict__ wr = reinterpret_cast<const double2*>(wr_ + o);
@@ -623,7 +629,7 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, 
   const int T = gridDim.x * blockDim.x;
   double acc[3] = {0.0, 0.0, 0.0};
   for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < npairs; c0 += XR2_U * T) {
-    double2 rv[XR2_U], pv[XR2_U], xv[XR2_U], av[XR2_U], bv[XR2_U], fv[XR2_U];
+    double2 rv[XR2_U], pv[XR2_U], av[XR2_U], bv[XR2_U], fv[XR2_U];
     bool okx[XR2_U], oky[XR2_U];
 #pragma unroll
     for (int u = 0; u < XR2_U; ++u) {
@@ -632,7 +638,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, 
       const double2 z = make_double2(0.0, 0.0);
       rv[u] = ok ? rr[c] : z;
       pv[u] = ok ? pr[c] : z;
-      xv[u] = ok ? xr[c] : z;
       av[u] = ok ? wr[c] : z;
       bv[u] = ok ? wc[c] : z;
       const int e = 2 * c, j = e >> lgp, i = e & (pitch - 1);
@@ -651,7 +656,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, 
       if (c < npairs) {
         pr[c] = p;
         rr[c] = r;
-        xr[c] = make_double2(fma(al, p.x, xv[u].x), fma(al, p.y, xv[u].y));
       }
       acc[1] = fma(r.x, r.x, fma(r.y, r.y, acc[1]));
       acc[2] = fma(r.x * r.x, iF.x, fma(r.y * r.y, iF.y, acc[2]));
@@ -688,7 +692,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
   const size_t o = (size_t)rhs * ((size_t)n << lgp);
   const int nq = (n << lgp) >> 2;
   const double al = k.st[rhs].alpha, be = k.st[rhs].betac;
-  double* __restrict__ xr = k.x + o;
   double* __restrict__ rr = k.r + o;
   double* __restrict__ pr = k.p + o;
   const double* __restrict__ wr = wr_ + o;
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
   const int T = gridDim.x * blockDim.x;
   double acc[3] = {0.0, 0.0, 0.0};
   for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < nq; c0 += U * T) {
-    dbl4 rv[U], pv[U], xv[U], av[U], bv[U];
+    dbl4 rv[U], pv[U], av[U], bv[U];
     double fy[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -705,7 +708,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
       const size_t e = (size_t)(ok ? c : 0) * 4;
       rv[u] = ld4(rr + e);
       pv[u] = ld4(pr + e);
-      xv[u] = ld4(xr + e);
       av[u] = ld4(wr + e);
       bv[u] = ld4(wc + e);
       fy[u] = Fy[(int)(e >> lgp)];
@@ -716,7 +718,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
       const int e = 4 * c, i = e & (pitch - 1);
       double* rp = &rv[u].x;
       double* pp = &pv[u].x;
-      double* xp = &xv[u].x;
       const double* ap = &av[u].x;
       const double* bp = &bv[u].x;
 #pragma unroll
@@ -727,7 +728,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
         const double q = ok ? ap[s] + bp[s] : 0.0;
         const double r = fma(-al, q, rp[s]);
         pp[s] = pn;
-        xp[s] = fma(al, pn, xp[s]);
         rp[s] = r;
         acc[1] = fma(r, r, acc[1]);
         acc[2] = fma(r * r, iF, acc[2]);
@@ -735,11 +735,31 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
       if (c < nq) {
         st4(pr + (size_t)e, pv[u]);
         st4(rr + (size_t)e, rv[u]);
-        st4(xr + (size_t)e, xv[u]);
       }
     }
   }
   kry_reduce_finalize(k, acc);
+}
+
+// end of a concurrent-body solve: the lagged x̂ += α p̂ of the last iteration
+// (α = 0 after a breakdown exit, so nothing is pending then)
+__global__ void __launch_bounds__(256) k_sine_xfix(KryFuse k, int n, int lgp) {
+  FDE_PDL_ENTRY();
+  const int rhs = blockIdx.y;
+  const size_t o = (size_t)rhs * ((size_t)n << lgp);
+  const int nq = (n << lgp) >> 2;
+  const double al = k.st[rhs].alpha;
+  if (al == 0.0) return;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nq; c += gridDim.x * blockDim.x) {
+    const size_t e = (size_t)c * 4;
+    dbl4 xv = ld4(k.x + o + e);
+    const dbl4 pv = ld4(k.p + o + e);
+    xv.x = fma(al, pv.x, xv.x);
+    xv.y = fma(al, pv.y, xv.y);
+    xv.z = fma(al, pv.z, xv.z);
+    xv.w = fma(al, pv.w, xv.w);
+    st4(k.x + o + e, xv);
+  }
 }
 
 // sine-domain PCG start: x̂ = 0, p̂ = 0, ‖b̂‖, ρ = Σ r̂²/F, β = 0 (r̂ = b̂ already formed)
