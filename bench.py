@@ -90,14 +90,14 @@ def unit_counts(name: str, p) -> tuple:
         # sine-domain operator line pass: DST, Toeplitz, DST on each
         # line; rows: read r, p, write p, w; cols: read p, w, write q; 1D: read r, p,
         # write p, q; concurrent body (rc): rows AND columns, each reading r, p_old and
-        # writing its w; the row units also apply the lagged x += αp (read, write x)
-        b = {"sine_op_rows": 32, "sine_op_cols": 24, "sine_op_1d": 32, "sine_op_rc": 64}[name]
+        # writing its w; the row units also write p_new and apply the lagged x += αp
+        b = {"sine_op_rows": 32, "sine_op_cols": 24, "sine_op_1d": 32, "sine_op_rc": 72}[name]
         f_line = 2 * 2.5 * m * lg + (10 * m * lg + 2 * m + 2 * n) + 3 * n
         return b * el, f_line * lines * (2 if name == "sine_op_rc" else 1)
     if name == "sine_xr":
         return 48 * el, 8 * el   # read x, p, r, q; write x, r
     if name == "sine_xr_rc":
-        return 48 * el, 10 * el  # read r, p, w_r, w_c; write p, r (x is updated, lagged, by the row units)
+        return 32 * el, 7 * el   # read r, w_r, w_c; write r (p and the lagged x are written by the row units)
     if name.startswith("pcg_"):
         return 48 * el, 6 * el
     raise KeyError(name)

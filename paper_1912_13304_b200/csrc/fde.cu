@@ -290,6 +290,7 @@ struct fde_handle_s {
   Counters* ctr = nullptr;
   double* part = nullptr;
   double *kx = nullptr, *kb = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kq = nullptr;
+  double* kp2 = nullptr;    // second p̂ buffer of the concurrent sine body
   double* kpart = nullptr;  // fused-kernel partials [batch][3][KPMAX]
   double2* zscr = nullptr;  // variable Toeplitz spectrum scratch [batch][pairs][L]
   double* V = nullptr;
@@ -1133,6 +1134,7 @@ void ensure_krylov(fde_handle h, int nvecV) {
     h->kz = h->dalloc<double>(ve);
     h->kp = h->dalloc<double>(vs);
     h->kq = h->dalloc<double>(vs);
+    h->kp2 = h->dalloc<double>(vs);
     h->kpart = h->dalloc<double>((size_t)h->batch * 3 * KPMAX);
   }
   if (nvecV > h->V_cols) {
@@ -1209,6 +1211,7 @@ void pcg_iteration(fde_handle h, const VecArgs& va) {
   kf.x = h->kx;
   kf.r = h->kr;
   kf.q = h->kq;
+  kf.p2 = h->kp2;
   kf.st = h->sst;
   kf.ctr = h->ctr;
   kf.part = h->kpart;
@@ -1232,6 +1235,7 @@ KryFuse make_kf(fde_handle h, double rtol, int maxit) {
   kf.x = h->kx;
   kf.r = h->kr;
   kf.q = h->kq;
+  kf.p2 = h->kp2;
   kf.st = h->sst;
   kf.ctr = h->ctr;
   kf.part = h->kpart;
@@ -1314,7 +1318,7 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     a.y = h->wx;
     a.mu = h->mus_xn;
     a.kf = kf;
-    a.kf.mode = KM_PQ | KM_PQS | KM_GATE;
+    a.kf.mode = KM_PQ | KM_PQS | KM_GATE | KM_PFLIP;
     LineArgs c = a;
     c.y = h->wy;
     c.mu = h->mus_y;

@@ -38,6 +38,7 @@ struct SolveState {          // one per RHS, device resident
   int kused;                 // GMRES: steps taken in the current cycle
   int restarts;
   int kbody;                 // sine-domain PCG: loop bodies started (body k forms r_k)
+  int ppar;                  // concurrent sine body: p̂_old lives in KryFuse::p (0) or p2 (1)
 };
 
 struct GmresSmall {          // one per RHS
@@ -679,7 +680,11 @@ __global__ void k_gm_restart(VecArgs a, const double* __restrict__ b, const doub
 //   KM_PQX   store the CTA's slot-0 partial in the extra region
 //            kpart[(rhs*3)*KPMAX + KPMAX/2 + blockIdx.x] and stop (no ticket);
 //            a later KM_PQ pass with KryFuse::xpart = that grid size adds them
-enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16, KM_INIT = 32, KM_SROW = 64, KM_PQS = 128, KM_PQX = 256 };
+//   KM_PFLIP the finalising CTA swaps the concurrent sine body's p̂ buffers
+//            (SolveState::ppar): the row units write p̂_new into the other
+//            buffer while the column units still read p̂_old
+enum { KM_PUPD = 1, KM_PQ = 2, KM_XR = 4, KM_RZ = 8, KM_GATE = 16, KM_INIT = 32, KM_SROW = 64, KM_PQS = 128, KM_PQX = 256,
+       KM_PFLIP = 512 };
 constexpr int KPMAX = 4096;   // CTAs per RHS of one line kernel
 
 struct KryFuse {
@@ -688,6 +693,7 @@ struct KryFuse {
   double* x;
   double* r;
   double* q;
+  double* p2;   // second p̂ buffer of the concurrent sine body (KM_PFLIP)
   SolveState* st;
   Counters* ctr;
   double* part;
@@ -761,6 +767,7 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
     s.betac = 0.0;
     s.alpha = 0.0;
     s.kbody = 0;
+    s.ppar = 0;
     s.iters = 0;
     s.converged = 0;
     s.status = ST_OK;
@@ -813,6 +820,7 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
       finish_rhs(k.ctr, s);
     } else {
       s.alpha = s.rho / pq;
+      if (k.mode & KM_PFLIP) s.ppar ^= 1;
     }
   }
   if (k.mode & KM_XR) {

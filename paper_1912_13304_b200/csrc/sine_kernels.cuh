@@ -90,7 +90,8 @@ __device__ __forceinline__ double symbol_at(const LineArgs& a, int l, int e) {
 // the fly (not written back), apply their direction's operator and write it
 // (6: w_r = ν p̂ + (S T̃_α S) p̂ rows, ν in μ; 7: w_c = (S T̃_β S) p̂ columns);
 // p̂·q̂ = p̂·w_r + p̂·w_c from the spectra (KM_PQS), α by the launch's last CTA.
-// k_sine_xr3 then writes p̂ and forms q̂ = w_r + w_c for the vector step.
+// the row units also write p̂ (into the other p̂ buffer: SolveState::ppar) and
+// apply the lagged x̂ update; k_sine_xr3/4 form q̂ = w_r + w_c for the vector step.
 template <int KM, bool COL, int FPC, int MODE>
 __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
   using GD = FftGeom<KM, sine_kd(KM)>;           // DST: length-m FFT, 2^KD points per thread
@@ -122,6 +123,11 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
   // 1. stage the operator input in shared memory (natural order)
   SolveState* const sst = a.kf.st + blockIdx.y;
   const double beta = (MODE == 0 || MODE == 2 || MODE == 6 || MODE == 7) ? sst->betac : 0.0;
+  // MODE 6/7 read p̂_old from the buffer SolveState::ppar names; MODE 6 writes
+  // p̂_new into the other one (the column units read p̂_old concurrently)
+  const int ppar = (MODE >= 6) ? sst->ppar : 0;
+  const double* const pold = (MODE >= 6 && ppar) ? a.kf.p2 : a.kf.p;
+  double* const pnew = (MODE >= 6 && ppar) ? a.kf.p : a.kf.p2;
   // MODE 6 applies the lagged x̂ += α_{k-1} p̂_{k-1} (k_sine_xr3/4 leave x̂ alone)
   const double alpha = (MODE == 3 || MODE == 5 || MODE == 6) ? sst->alpha : 0.0;
   double acc[3] = {0.0, 0.0, 0.0};
@@ -138,8 +144,9 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
       const long long o0 = A0.base + (long long)(ok ? e : 0) * A0.stride, o1 = A1.base + (long long)(ok ? e : 0) * A1.stride;
       const double* src[4];
       if (MODE == 3 || MODE == 5) { src[0] = a.kf.r; src[1] = a.kf.q; src[2] = a.kf.p; src[3] = a.kf.x; }
-      else if (MODE == 6) { src[0] = a.x; src[1] = a.kf.p; src[2] = a.kf.x; }
-      else if (MODE == 0 || MODE == 2 || MODE == 7) { src[0] = a.x; src[1] = a.kf.p; }
+      else if (MODE == 6) { src[0] = a.x; src[1] = pold; src[2] = a.kf.x; }
+      else if (MODE == 7) { src[0] = a.x; src[1] = pold; }
+      else if (MODE == 0 || MODE == 2) { src[0] = a.x; src[1] = a.kf.p; }
       else if (MODE == 4) { src[0] = a.kf.r; }
       else { src[0] = a.x; }
 #pragma unroll
@@ -172,12 +179,18 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
         p1 = fma(beta, g1v[1][i], g1v[0][i] * fast_rcp(f1v[i]));
         if (v0) a.kf.p[o0] = p0;
         if (v1) a.kf.p[o1] = p1;
-      } else if (MODE >= 6) {  // p̂ = ẑ + β p̂_old, kept on chip (k_sine_xr3 writes it)
+      } else if (MODE >= 6) {  // p̂ = ẑ + β p̂_old
         p0 = fma(beta, g0v[1][i], g0v[0][i] * fast_rcp(f0v[i]));
         p1 = fma(beta, g1v[1][i], g1v[0][i] * fast_rcp(f1v[i]));
-        if (MODE == 6) {  // lagged x̂ update of the previous iteration (rows: coalesced)
-          if (v0) a.kf.x[o0] = fma(alpha, g0v[1][i], g0v[NV - 1][i]);
-          if (v1) a.kf.x[o1] = fma(alpha, g1v[1][i], g1v[NV - 1][i]);
+        if (MODE == 6) {  // p̂_new and the lagged x̂ update of the previous iteration (rows: coalesced)
+          if (v0) {
+            pnew[o0] = p0;
+            a.kf.x[o0] = fma(alpha, g0v[1][i], g0v[NV - 1][i]);
+          }
+          if (v1) {
+            pnew[o1] = p1;
+            a.kf.x[o1] = fma(alpha, g1v[1][i], g1v[NV - 1][i]);
+          }
         }
       } else if (MODE == 3 || MODE == 5) {  // r̂ -= α q̂, x̂ += α p̂, ẑ = r̂/F
         const double r0 = fma(-alpha, g0v[1][i], g0v[0][i]), r1 = fma(-alpha, g1v[1][i], g1v[0][i]);
@@ -607,11 +620,11 @@ __global__ void __launch_bounds__(256) k_sine_xr2(KryFuse k, int n, int lgp, con
   kry_reduce_finalize(k, acc);
 }
 
-// vector step of the concurrent body (after k_sineop_rc): p̂ = r̂/F + β p̂_old
-// (written), q̂ = w_r + w_c, r̂ -= α q̂, partials ‖r̂‖², r̂·ẑ. x̂ += α p̂ is
-// lagged: the next row pass applies it (k_sine_xfix after the last iteration). Flat over
-// the internal layout like k_sine_xr2; padding entries (i >= n) of w_r, w_c are
-// never written, so they are masked here.
+// vector step of the concurrent body (after k_sineop_rc, whose row units wrote
+// p̂_new and applied the lagged x̂ += α_{k-1} p̂_{k-1}): q̂ = w_r + w_c,
+// r̂ -= α q̂, partials ‖r̂‖², r̂·ẑ (k_sine_xfix adds the last α p̂ after the
+// loop). Flat over the internal layout like k_sine_xr2; padding entries
+// (i >= n) of w_r, w_c are never written, so they are masked here.
 __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, const double* __restrict__ Fx,
                                                   const double* __restrict__ Fy, const double* __restrict__ wr_,
                                                   const double* __restrict__ wc_) {
@@ -621,15 +634,14 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, 
   const int pitch = 1 << lgp;
   const size_t o = (size_t)rhs * ((size_t)n << lgp);
   const int npairs = (n << lgp) >> 1;
-  const double al = k.st[rhs].alpha, be = k.st[rhs].betac;
+  const double al = k.st[rhs].alpha;
   double2* __restrict__ rr = reinterpret_cast<double2*>(k.r + o);
-  double2* __restrict__ pr = reinterpret_cast<double2*>(k.p + o);
   const double2* __restrict__ wr = reinterpret_cast<const double2*>(wr_ + o);
   const double2* __restrict__ wc = reinterpret_cast<const double2*>(wc_ + o);
   const int T = gridDim.x * blockDim.x;
   double acc[3] = {0.0, 0.0, 0.0};
   for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < npairs; c0 += XR2_U * T) {
-    double2 rv[XR2_U], pv[XR2_U], av[XR2_U], bv[XR2_U], fv[XR2_U];
+    double2 rv[XR2_U], av[XR2_U], bv[XR2_U], fv[XR2_U];
     bool okx[XR2_U], oky[XR2_U];
 #pragma unroll
     for (int u = 0; u < XR2_U; ++u) {
@@ -637,7 +649,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, 
       const bool ok = c < npairs;
       const double2 z = make_double2(0.0, 0.0);
       rv[u] = ok ? rr[c] : z;
-      pv[u] = ok ? pr[c] : z;
       av[u] = ok ? wr[c] : z;
       bv[u] = ok ? wc[c] : z;
       const int e = 2 * c, j = e >> lgp, i = e & (pitch - 1);
@@ -650,13 +661,9 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, 
     for (int u = 0; u < XR2_U; ++u) {
       const int c = c0 + u * T;
       const double2 iF = make_double2(fast_rcp(fv[u].x), fast_rcp(fv[u].y));
-      const double2 p = make_double2(fma(be, pv[u].x, rv[u].x * iF.x), fma(be, pv[u].y, rv[u].y * iF.y));
       const double2 q = make_double2(okx[u] ? av[u].x + bv[u].x : 0.0, oky[u] ? av[u].y + bv[u].y : 0.0);
       const double2 r = make_double2(fma(-al, q.x, rv[u].x), fma(-al, q.y, rv[u].y));
-      if (c < npairs) {
-        pr[c] = p;
-        rr[c] = r;
-      }
+      if (c < npairs) rr[c] = r;
       acc[1] = fma(r.x, r.x, fma(r.y, r.y, acc[1]));
       acc[2] = fma(r.x * r.x, iF.x, fma(r.y * r.y, iF.y, acc[2]));
     }
@@ -691,15 +698,14 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
   const int pitch = 1 << lgp;
   const size_t o = (size_t)rhs * ((size_t)n << lgp);
   const int nq = (n << lgp) >> 2;
-  const double al = k.st[rhs].alpha, be = k.st[rhs].betac;
+  const double al = k.st[rhs].alpha;
   double* __restrict__ rr = k.r + o;
-  double* __restrict__ pr = k.p + o;
   const double* __restrict__ wr = wr_ + o;
   const double* __restrict__ wc = wc_ + o;
   const int T = gridDim.x * blockDim.x;
   double acc[3] = {0.0, 0.0, 0.0};
   for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < nq; c0 += U * T) {
-    dbl4 rv[U], pv[U], av[U], bv[U];
+    dbl4 rv[U], av[U], bv[U];
     double fy[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -707,7 +713,6 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
       const bool ok = c < nq;
       const size_t e = (size_t)(ok ? c : 0) * 4;
       rv[u] = ld4(rr + e);
-      pv[u] = ld4(pr + e);
       av[u] = ld4(wr + e);
       bv[u] = ld4(wc + e);
       fy[u] = Fy[(int)(e >> lgp)];
@@ -717,25 +722,19 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
       const int c = c0 + u * T;
       const int e = 4 * c, i = e & (pitch - 1);
       double* rp = &rv[u].x;
-      double* pp = &pv[u].x;
       const double* ap = &av[u].x;
       const double* bp = &bv[u].x;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const bool ok = i + s < n;
         const double iF = fast_rcp(ok ? Fx[i + s] + fy[u] : 1.0);
-        const double pn = fma(be, pp[s], rp[s] * iF);
         const double q = ok ? ap[s] + bp[s] : 0.0;
         const double r = fma(-al, q, rp[s]);
-        pp[s] = pn;
         rp[s] = r;
         acc[1] = fma(r, r, acc[1]);
         acc[2] = fma(r * r, iF, acc[2]);
       }
-      if (c < nq) {
-        st4(pr + (size_t)e, pv[u]);
-        st4(rr + (size_t)e, rv[u]);
-      }
+      if (c < nq) st4(rr + (size_t)e, rv[u]);
     }
   }
   kry_reduce_finalize(k, acc);
@@ -753,7 +752,7 @@ __global__ void __launch_bounds__(256) k_sine_xfix(KryFuse k, int n, int lgp) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nq; c += gridDim.x * blockDim.x) {
     const size_t e = (size_t)c * 4;
     dbl4 xv = ld4(k.x + o + e);
-    const dbl4 pv = ld4(k.p + o + e);
+    const dbl4 pv = ld4((k.st[rhs].ppar ? k.p2 : k.p) + o + e);
     xv.x = fma(al, pv.x, xv.x);
     xv.y = fma(al, pv.y, xv.y);
     xv.z = fma(al, pv.z, xv.z);
@@ -785,6 +784,7 @@ __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, c
         k.x[e] = 0.0;
         k.p[e] = 0.0;
         k.q[e] = 0.0;
+        if (k.p2) k.p2[e] = 0.0;
       }
   }
   // reuse the fused finalisation: slot 1 -> ‖b̂‖, slot 2 -> ρ (mode bits select the init path)
