@@ -304,6 +304,7 @@ struct fde_handle_s {
   int g_maxit = -1;
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
+  bool gm_dcgs = true;              // GMRES orthogonalisation by DCGS2 (FDE_GM_ORTH=cgs2: classical CGS2)
   bool gm_ws = true;                // warp-split CGS kernels for j < 32 (FDE_GM_WS=0: one thread per element)
   bool sine_xr4 = true;             // 32-byte vector step of the concurrent body (FDE_XR4=0: 16-byte)
   bool sine_xr_rows = false;        // FDE_SINE_XR=rows: the per-row vector step instead of the flat one
@@ -992,6 +993,8 @@ void build(fde_handle h, const fde_desc* d) {
     // DESIGN.md §5.4); FDE_SINE_RC=1 / 0 forces it on / off
     const char* rc = std::getenv("FDE_SINE_RC");
     h->sine_rc = rc ? std::strcmp(rc, "0") != 0 : (h->batch == 1 && n <= 2047);
+    const char* go = std::getenv("FDE_GM_ORTH");
+    h->gm_dcgs = !(go && std::strcmp(go, "cgs2") == 0);
     const char* gw = std::getenv("FDE_GM_WS");
     h->gm_ws = !(gw && std::strcmp(gw, "0") == 0);
     const char* x4 = std::getenv("FDE_XR4");
@@ -1507,6 +1510,42 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
   const int* gU = &h->ctr->unfinished;
   const size_t vs = h->vec_elems();
   double* V = h->V;
+  if (h->gm_dcgs && restart <= 31) {  // DCGS2: two passes over the basis per step (krylov_kernels.cuh)
+    auto pick = [&](int j, auto&& f) {
+      if (j < 8) f(std::integral_constant<int, 1>{}, std::integral_constant<int, 16>{});
+      else if (j < 16) f(std::integral_constant<int, 2>{}, std::integral_constant<int, 8>{});
+      else f(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{});
+    };
+    for (int j = 0; j <= restart; ++j) {
+      double* Vj = V + (size_t)j * vs;
+      if (j == restart) {  // end of cycle: reorthogonalise u_m, finalise column m-1
+        pick(j, [&](auto NS, auto EPL) {
+          launch_named(h, "gm_dcgs_a", [&] {
+            launch_k(h->st, k_gm_dcgs_a<decltype(NS)::value, decltype(EPL)::value>, VGRID, RED_THREADS, 0, va, V, vs,
+                     (const double*)Vj, (const double*)nullptr, j);
+          });
+        });
+        break;
+      }
+      double* Vn = V + (size_t)(j + 1) * vs;
+      if (!left) {
+        op_tau(h, Vj, h->kz, gA);
+        op_matvec(h, h->kz, Vn, gA);
+      } else {
+        op_matvec(h, Vj, h->kq, gA);
+        op_tau(h, h->kq, Vn, gA);
+      }
+      pick(j, [&](auto NS, auto EPL) {
+        constexpr int ns = decltype(NS)::value, epl = decltype(EPL)::value;
+        launch_named(h, "gm_dcgs_a", [&] {
+          launch_k(h->st, k_gm_dcgs_a<ns, epl>, VGRID, RED_THREADS, 0, va, V, vs, (const double*)Vj, (const double*)Vn, j);
+        });
+        launch_named(h, "gm_dcgs_b", [&] {
+          launch_k(h->st, k_gm_dcgs_b<ns, epl>, VGRID, RED_THREADS, 0, va, V, vs, Vj, Vn, j);
+        });
+      });
+    }
+  } else
   for (int j = 0; j < restart; ++j) {  // basis vectors stay unnormalised (GmresSmall::vsc)
     double* Vj = V + (size_t)j * vs;
     double* Vn = V + (size_t)(j + 1) * vs;

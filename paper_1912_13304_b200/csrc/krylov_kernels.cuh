@@ -51,6 +51,10 @@ struct GmresSmall {          // one per RHS
   // (so no separate scaling pass over the new vector; the factors enter the
   // dot and update coefficients)
   double vsc[MAX_RESTART + 1];
+  // DCGS2 (delayed reorthogonalisation, k_gm_dcgs_*): the unrotated Arnoldi
+  // Hessenberg and the pass-B coefficients of the current step
+  double Hr[(MAX_RESTART + 1) * MAX_RESTART];
+  double dj, binv;
 };
 
 struct Counters {            // device counters
@@ -568,6 +572,268 @@ __global__ void __launch_bounds__(256) k_gm_cgs_ws(VecArgs a, const double* __re
       finalize(part, 1, out);
       if (threadIdx.x == 0) arnoldi_step(a, rb, j, out[0]);
     }
+  }
+}
+
+// ================================================ DCGS2 (delayed CGS2) =====
+// Classical Gram-Schmidt with delayed reorthogonalisation: the candidate u_j
+// (w_{j-1} after ONE projection) is reorthogonalised at step j, in the same
+// reduction as the first projection of z = A P⁻¹ u_j, so a step makes two
+// passes over the basis instead of CGS2's three:
+//   pass A: a = Vᵀu_j, b = Vᵀz, ν = u_jᵀu_j, c = u_jᵀz            (one reduction)
+//           β_j = sqrt(ν - aᵀa), column j-1: H[:, j-1] += a, H[j, j-1] = β_j,
+//           Givens on column j-1 (convergence after j Arnoldi steps);
+//           d = [b, (c - aᵀb)/β_j], new column j: h = (d - H a)/β_j
+//   pass B: q_j = (u_j - V a)/β_j ; u_{j+1} = (z - V b - d_j q_j)/β_j
+// Exact arithmetic gives the Arnoldi relation of CGS2 (A P⁻¹ q_j = V h + u_{j+1}
+// with V orthonormal); the cycle ends with one pass A without z for column m-1.
+// Partial slots: a_i at i, b_i at j+i, ν at 2j, c at 2j+1 (2j+2 <= 64: j <= 31).
+
+// the finalising block of pass A (all its threads; sums in gs.h[0 .. 2j+1]):
+// thread 0 finalises column j-1 (O(j) serial, on register copies), the
+// block forms the new raw column j in parallel
+__device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z) {
+  SolveState& s = a.st[rb];
+  GmresSmall& gs = a.gs[rb];
+  constexpr int LD = MAX_RESTART + 1;
+  __shared__ double sa[32], sb[32];
+  __shared__ double s_bet;
+  __shared__ int s_stop;
+  for (int i = threadIdx.x; i < j; i += blockDim.x) {
+    sa[i] = __ldcg(&gs.h[i]);
+    sb[i] = __ldcg(&gs.h[j + i]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double nu = __ldcg(&gs.h[2 * j]);
+    double aa = 0.0;
+    for (int i = 0; i < j; ++i) aa = fma(sa[i], sa[i], aa);
+    const double bet2 = nu - aa;
+    const double bet = bet2 > 0.0 ? sqrt(bet2) : 0.0;
+    bool stop = false;
+    if (j >= 1) {  // finalise column j-1 and its Givens rotation
+      double* Hrc = gs.Hr + (size_t)(j - 1) * LD;
+      double* Hc = gs.H + (size_t)(j - 1) * LD;
+      double col[MAX_RESTART + 1];
+      for (int i = 0; i < j; ++i) {
+        col[i] = Hrc[i] + sa[i];
+        Hrc[i] = col[i];
+      }
+      col[j] = bet;
+      Hrc[j] = bet;
+      const int c = j - 1;
+      for (int i = 0; i < c; ++i) {
+        const double ci = gs.cs[i], si = gs.sn[i];
+        const double t = ci * col[i] + si * col[i + 1];
+        col[i + 1] = -si * col[i] + ci * col[i + 1];
+        col[i] = t;
+      }
+      const double den = hypot(col[c], col[c + 1]);
+      const double cn = col[c] / den, sn = col[c + 1] / den;
+      gs.cs[c] = cn;
+      gs.sn[c] = sn;
+      col[c] = den;
+      col[c + 1] = 0.0;
+      for (int i = 0; i <= j; ++i) Hc[i] = col[i];
+      const double gc = gs.g[c];
+      gs.g[c + 1] = -sn * gc;
+      gs.g[c] = cn * gc;
+      s.iters += 1;
+      s.kused = j;
+      s.rnorm = fabs(sn * gc) / s.bnorm;
+      if (!isfinite(bet) || !isfinite(den)) {
+        s.status = ST_NONFINITE;
+        stop = true;
+      } else if (fabs(sn * gc) <= a.rtol * s.bnorm) {
+        s.converged = 1;
+        stop = true;
+      } else if (bet == 0.0) {
+        s.status = ST_BREAKDOWN;
+        stop = true;
+      } else if (s.iters >= a.maxit || !has_z) {
+        stop = true;  // budget, or the end-of-cycle pass
+      }
+    } else if (!(bet > 0.0)) {
+      s.status = isfinite(bet) ? ST_BREAKDOWN : ST_NONFINITE;
+      stop = true;
+    }
+    if (stop && s.cyc_active) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
+    s_bet = bet;
+    s_stop = stop;
+  }
+  __syncthreads();
+  if (s_stop) return;
+  // pass-B coefficients and the first projection (new raw column j):
+  // d = [b, (c - aᵀb)/β], Hr[:, j] = (d - H a)/β with the finalised columns k < j
+  const double bi = 1.0 / s_bet;
+  const double cc = has_z ? __ldcg(&gs.h[2 * j + 1]) : 0.0;
+  double ab = 0.0;
+  for (int i = 0; i < j; ++i) ab = fma(sa[i], sb[i], ab);
+  const double dj = (cc - ab) * bi;
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+    double ha = 0.0;  // upper Hessenberg: Hr[i][k] != 0 for k >= i-1
+    for (int k = (i > 0 ? i - 1 : 0); k < j; ++k) ha = fma(__ldcg(&gs.Hr[(size_t)k * LD + i]), sa[k], ha);
+    const double di = i < j ? sb[i] : dj;
+    gs.Hr[(size_t)j * LD + i] = (di - ha) * bi;
+    if (i < j) {
+      gs.h2[i] = sa[i];
+      gs.h2[32 + i] = sb[i];
+    }
+  }
+  if (threadIdx.x == 0) {
+    gs.dj = dj;
+    gs.binv = bi;
+    gs.vsc[j] = 1.0;  // q_j is stored normalised by pass B
+  }
+}
+
+// pass A (z == nullptr: the end-of-cycle pass, a and ν only)
+template <int NS, int EPL>
+__global__ void __launch_bounds__(256) k_gm_dcgs_a(VecArgs a, const double* __restrict__ V, size_t vstride,
+                                                   const double* __restrict__ u, const double* __restrict__ z, int j) {
+  FDE_PDL_ENTRY();
+  constexpr int CH = 32 * EPL;
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  const int nv = j;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ double su[CH], sz[CH];
+  constexpr int TPT = (CH + 255) / 256;
+  double acc_a[NS], acc_b[NS];
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) acc_a[sl] = acc_b[sl] = 0.0;
+  double nu = 0.0, cc = 0.0;
+  const bool hz = z != nullptr;
+  for (long long c0 = (long long)blockIdx.x * CH; c0 < N; c0 += (long long)gridDim.x * CH) {
+    double vv[NS][EPL];
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int i = wid + 8 * sl;
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        const long long e = c0 + lane + 32 * q;
+        vv[sl][q] = (i < nv && e < N) ? __ldg(V + (size_t)i * vstride + o + e) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      const int t = threadIdx.x + 256 * q;
+      if (t < CH) {
+        const long long e = c0 + t;
+        const double uv = e < N ? u[o + e] : 0.0;
+        const double zv = (hz && e < N) ? z[o + e] : 0.0;
+        su[t] = uv;
+        sz[t] = zv;
+        nu = fma(uv, uv, nu);
+        cc = fma(uv, zv, cc);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl)
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        acc_a[sl] = fma(vv[sl][q], su[lane + 32 * q], acc_a[sl]);
+        acc_b[sl] = fma(vv[sl][q], sz[lane + 32 * q], acc_b[sl]);
+      }
+    __syncthreads();
+  }
+  double* part = a.part + (size_t)rb * (MAX_RESTART + 1) * RED_BLOCKS;
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) {
+    const int i = wid + 8 * sl;
+    const double va = warp_sum(acc_a[sl]), vb = warp_sum(acc_b[sl]);
+    if (lane == 0 && i < nv) {
+      part[(size_t)i * RED_BLOCKS + blockIdx.x] = va;
+      part[(size_t)(j + i) * RED_BLOCKS + blockIdx.x] = vb;
+    }
+  }
+  __shared__ double red[2 * 32];
+  double nc[2] = {nu, cc};
+  block_sum<2>(nc, red);
+  if (threadIdx.x == 0) {
+    part[(size_t)(2 * j) * RED_BLOCKS + blockIdx.x] = nc[0];
+    part[(size_t)(2 * j + 1) * RED_BLOCKS + blockIdx.x] = nc[1];
+  }
+  if (last_block(&a.ctr->tickets[rb * 8])) {
+    finalize(part, 2 * j + 2, a.gs[rb].h);
+    dcgs_step(a, rb, j, hz);
+  }
+}
+
+// pass B: q_j (into u's slot) and u_{j+1} (into z's slot)
+template <int NS, int EPL0>
+__global__ void __launch_bounds__(256) k_gm_dcgs_b(VecArgs a, const double* __restrict__ V, size_t vstride,
+                                                   double* __restrict__ u, double* __restrict__ z, int j) {
+  FDE_PDL_ENTRY();
+  constexpr int EPL = EPL0 > 8 ? 8 : EPL0;  // two 8 x CH partial arrays in 48 KB of static shared memory
+  constexpr int CH = 32 * EPL;
+  if (a.ctr->active == 0) return;
+  const int rb = blockIdx.y, N = a.N;
+  if (!a.st[rb].cyc_active) return;
+  const size_t o = (size_t)rb * N;
+  const int nv = j;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ double pa[8][CH], pb[8][CH];
+  __shared__ double ca[32], cb[32];
+  const GmresSmall& gs = a.gs[rb];
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) {
+    ca[i] = i < nv ? __ldcg(&gs.h2[i]) : 0.0;
+    cb[i] = i < nv ? __ldcg(&gs.h2[32 + i]) : 0.0;
+  }
+  const double dj = __ldcg(&gs.dj), bi = __ldcg(&gs.binv);
+  __syncthreads();
+  constexpr int TPT = (CH + 255) / 256;
+  for (long long c0 = (long long)blockIdx.x * CH; c0 < N; c0 += (long long)gridDim.x * CH) {
+    double vv[NS][EPL];
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int i = wid + 8 * sl;
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        const long long e = c0 + lane + 32 * q;
+        vv[sl][q] = (i < nv && e < N) ? __ldg(V + (size_t)i * vstride + o + e) : 0.0;
+      }
+    }
+    double uv[TPT], zv[TPT];
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      const int t = threadIdx.x + 256 * q;
+      const long long e = c0 + t;
+      uv[q] = (t < CH && e < N) ? u[o + e] : 0.0;
+      zv[q] = (t < CH && e < N) ? z[o + e] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) {
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        sa = fma(ca[wid + 8 * sl], vv[sl][q], sa);
+        sb = fma(cb[wid + 8 * sl], vv[sl][q], sb);
+      }
+      pa[wid][lane + 32 * q] = sa;
+      pb[wid][lane + 32 * q] = sb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      const int t = threadIdx.x + 256 * q;
+      const long long e = c0 + t;
+      if (t < CH && e < N) {
+        double SA = 0.0, SB = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          SA += pa[k][t];
+          SB += pb[k][t];
+        }
+        const double qv = (uv[q] - SA) * bi;
+        u[o + e] = qv;
+        z[o + e] = (zv[q] - SB - dj * qv) * bi;
+      }
+    }
+    __syncthreads();
   }
 }
 

@@ -78,10 +78,13 @@ def test_solver_parity(torch_cuda, cfg, n, batch, solver, prec):
         assert np.linalg.norm(r) / np.linalg.norm(p.rhs[b]) <= 1e-9
 
 
-@pytest.mark.parametrize("ws", ["0", "1"])
-def test_gmres_cgs_kernel_variants(torch_cuda, monkeypatch, ws):
-    """Both CGS2 kernel families (FDE_GM_WS=1: warp-split passes, the default
-    for j < 32; 0: one thread per element) match the oracle's GMRES(30)."""
+@pytest.mark.parametrize("orth,ws", [("dcgs2", "1"), ("cgs2", "1"), ("cgs2", "0")])
+def test_gmres_cgs_kernel_variants(torch_cuda, monkeypatch, orth, ws):
+    """Every orthogonalisation path matches the oracle's GMRES(30) (CGS2):
+    DCGS2 (the default for restart <= 31: delayed reorthogonalisation, two
+    passes over the basis per step), and CGS2 with warp-split (FDE_GM_WS=1) or
+    one-thread-per-element (0) kernels."""
+    monkeypatch.setenv("FDE_GM_ORTH", orth)
     monkeypatch.setenv("FDE_GM_WS", ws)
     for cfg, n, batch, prec in ((2, 255, 2, W.PREC_TAU_D), (4, 127, 1, W.PREC_TAU)):
         p = W.config(cfg, n=n, batch=batch, prec=prec)
@@ -91,8 +94,8 @@ def test_gmres_cgs_kernel_variants(torch_cuda, monkeypatch, ws):
         for b in range(batch):
             xo, it_o, conv_o, _ = ref[b]
             assert stats[b]["converged"] and conv_o
-            assert abs(stats[b]["iters"] - it_o) <= 1, (ws, b, stats[b]["iters"], it_o)
-            assert relerr(x[b], xo) <= 1e-9, (ws, relerr(x[b], xo))
+            assert abs(stats[b]["iters"] - it_o) <= 1, (orth, ws, b, stats[b]["iters"], it_o)
+            assert relerr(x[b], xo) <= 1e-9, (orth, ws, relerr(x[b], xo))
 
 
 def test_gmres_left_unrestarted_matches_oracle(torch_cuda):
@@ -253,7 +256,8 @@ def test_profile_abis_report_every_kernel(torch_cuda):
     x = torch_cuda.zeros_like(b)
     live, _ = h.profile_solve(b, x, "gmres", 1e-10, 30, restart=5)
     names = [nm for nm, _ in live]
-    assert names.count("gm_upd_norm") == 5 and "toeplitz_rows_var" in names
+    # DCGS2: pass A per step plus the end-of-cycle pass A, pass B per step
+    assert names.count("gm_dcgs_a") == 6 and names.count("gm_dcgs_b") == 5 and "toeplitz_rows_var" in names
     h.close()
 
 
