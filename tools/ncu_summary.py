@@ -92,7 +92,7 @@ def _short(name):
         return {"0": "sine_op_rows", "1": "sine_op_cols", "2": "sine_op_1d"}[mode]
     if "k_sineop_rc" in n:
         return "sine_op_rc"
-    if "k_sine_xr3" in n:
+    if "k_sine_xr3" in n or "k_sine_xr4" in n:
         return "sine_xr_rc"
     if "k_sine_xr" in n:
         return "sine_xr"
