@@ -1510,6 +1510,10 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
   const int* gU = &h->ctr->unfinished;
   const size_t vs = h->vec_elems();
   double* V = h->V;
+  // grid of the chunked orthogonalisation kernels: one block per chunk up to
+  // RED_BLOCKS (small systems, e.g. 1D n = 4095, then finalise over a few
+  // partials instead of 592)
+  auto ggrid = [&](int chunk) { return dim3(std::min(RED_BLOCKS, std::max(1, (va.N + chunk - 1) / chunk)), h->batch); };
   if (h->gm_dcgs && restart <= 31) {  // DCGS2: two passes over the basis per step (krylov_kernels.cuh)
     auto pick = [&](int j, auto&& f) {
       if (j < 8) f(std::integral_constant<int, 1>{}, std::integral_constant<int, 16>{});
@@ -1521,8 +1525,8 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
       if (j == restart) {  // end of cycle: reorthogonalise u_m, finalise column m-1
         pick(j, [&](auto NS, auto EPL) {
           launch_named(h, "gm_dcgs_a", [&] {
-            launch_k(h->st, k_gm_dcgs_a<decltype(NS)::value, decltype(EPL)::value>, VGRID, RED_THREADS, 0, va, V, vs,
-                     (const double*)Vj, (const double*)nullptr, j);
+            launch_k(h->st, k_gm_dcgs_a<decltype(NS)::value, decltype(EPL)::value>, ggrid(32 * decltype(EPL)::value),
+                     RED_THREADS, 0, va, V, vs, (const double*)Vj, (const double*)nullptr, j);
           });
         });
         break;
@@ -1538,10 +1542,11 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
       pick(j, [&](auto NS, auto EPL) {
         constexpr int ns = decltype(NS)::value, epl = decltype(EPL)::value;
         launch_named(h, "gm_dcgs_a", [&] {
-          launch_k(h->st, k_gm_dcgs_a<ns, epl>, VGRID, RED_THREADS, 0, va, V, vs, (const double*)Vj, (const double*)Vn, j);
+          launch_k(h->st, k_gm_dcgs_a<ns, epl>, ggrid(32 * epl), RED_THREADS, 0, va, V, vs, (const double*)Vj,
+                   (const double*)Vn, j);
         });
         launch_named(h, "gm_dcgs_b", [&] {
-          launch_k(h->st, k_gm_dcgs_b<ns, epl>, VGRID, RED_THREADS, 0, va, V, vs, Vj, Vn, j);
+          launch_k(h->st, k_gm_dcgs_b<ns, epl>, ggrid(32 * (epl > 8 ? 8 : epl)), RED_THREADS, 0, va, V, vs, Vj, Vn, j);
         });
       });
     }
@@ -1557,14 +1562,15 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
       op_tau(h, h->kq, Vn, gA);
     }
     if (j < 32 && h->gm_ws) {  // warp-split CGS passes (krylov_kernels.cuh)
-      auto cgs = [&](auto k0, auto k1, auto k2) {
-        launch_named(h, "gm_mdot", [&] { launch_k(h->st, k0, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
-        launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k1, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
-        launch_named(h, "gm_upd_norm", [&] { launch_k(h->st, k2, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
+      auto cgs = [&](int chunk, auto k0, auto k1, auto k2) {
+        const dim3 gg = ggrid(chunk);
+        launch_named(h, "gm_mdot", [&] { launch_k(h->st, k0, gg, RED_THREADS, 0, va, V, vs, Vn, j); });
+        launch_named(h, "gm_upd_mdot", [&] { launch_k(h->st, k1, gg, RED_THREADS, 0, va, V, vs, Vn, j); });
+        launch_named(h, "gm_upd_norm", [&] { launch_k(h->st, k2, gg, RED_THREADS, 0, va, V, vs, Vn, j); });
       };
-      if (j < 8) cgs(k_gm_cgs_ws<0, 1, 16>, k_gm_cgs_ws<1, 1, 16>, k_gm_cgs_ws<2, 1, 16>);
-      else if (j < 16) cgs(k_gm_cgs_ws<0, 2, 8>, k_gm_cgs_ws<1, 2, 8>, k_gm_cgs_ws<2, 2, 8>);
-      else cgs(k_gm_cgs_ws<0, 4, 4>, k_gm_cgs_ws<1, 4, 4>, k_gm_cgs_ws<2, 4, 4>);
+      if (j < 8) cgs(512, k_gm_cgs_ws<0, 1, 16>, k_gm_cgs_ws<1, 1, 16>, k_gm_cgs_ws<2, 1, 16>);
+      else if (j < 16) cgs(256, k_gm_cgs_ws<0, 2, 8>, k_gm_cgs_ws<1, 2, 8>, k_gm_cgs_ws<2, 2, 8>);
+      else cgs(128, k_gm_cgs_ws<0, 4, 4>, k_gm_cgs_ws<1, 4, 4>, k_gm_cgs_ws<2, 4, 4>);
     } else {
       launch_named(h, "gm_mdot", [&] { launch_k(h->st, k_gm_mdot, VGRID, RED_THREADS, 0, va, V, vs, Vn, j); });
       if (j < 32)

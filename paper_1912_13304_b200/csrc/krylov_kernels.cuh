@@ -108,13 +108,13 @@ __device__ __forceinline__ bool last_block(unsigned* ticket) {
   return s_last;
 }
 
-// last block: out[i] = sum_bx part[(i)*RED_BLOCKS + bx] in fixed order (one warp per vector)
+// last block: out[i] = sum_bx part[(i)*RED_BLOCKS + bx], bx < gridDim.x (<= RED_BLOCKS), in fixed order (one warp per vector)
 __device__ __forceinline__ void finalize(const double* part, int nvec, double* out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = wid; i < nvec; i += nw) {
     double s = 0.0;
 #pragma unroll 8
-    for (int bx = lane; bx < RED_BLOCKS; bx += 32) s += __ldcg(part + (size_t)i * RED_BLOCKS + bx);
+    for (int bx = lane; bx < (int)gridDim.x; bx += 32) s += __ldcg(part + (size_t)i * RED_BLOCKS + bx);
     s = warp_sum(s);
     if (lane == 0) out[i] = s;
   }
