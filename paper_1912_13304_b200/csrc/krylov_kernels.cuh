@@ -110,13 +110,23 @@ __device__ __forceinline__ bool last_block(unsigned* ticket) {
 
 // last block: out[i] = sum_bx part[(i)*RED_BLOCKS + bx], bx < gridDim.x (<= RED_BLOCKS), in fixed order (one warp per vector)
 __device__ __forceinline__ void finalize(const double* part, int nvec, double* out) {
+  // each warp sums 8 vectors at once (their loads in flight together); per
+  // vector the order is the same fixed one: lane-strided over bx, then the warp
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = wid; i < nvec; i += nw) {
-    double s = 0.0;
-#pragma unroll 8
-    for (int bx = lane; bx < (int)gridDim.x; bx += 32) s += __ldcg(part + (size_t)i * RED_BLOCKS + bx);
-    s = warp_sum(s);
-    if (lane == 0) out[i] = s;
+  const int G = (int)gridDim.x;
+  for (int i0 = wid * 8; i0 < nvec; i0 += nw * 8) {
+    double sm8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+    for (int bx = lane; bx < G; bx += 32) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i0 + k < nvec) sm8[k] += __ldcg(part + (size_t)(i0 + k) * RED_BLOCKS + bx);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double v = warp_sum(sm8[k]);
+      if (lane == 0 && i0 + k < nvec) out[i0 + k] = v;
+    }
   }
   __syncthreads();
 }
@@ -596,16 +606,26 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
   SolveState& s = a.st[rb];
   GmresSmall& gs = a.gs[rb];
   constexpr int LD = MAX_RESTART + 1;
-  __shared__ double sa[32], sb[32];
-  __shared__ double s_bet;
+  __shared__ double sa[32], sb[32], scs[32], ssn[32], scol[33];
+  __shared__ double s_bet, s_nu, s_g;
   __shared__ int s_stop;
-  for (int i = threadIdx.x; i < j; i += blockDim.x) {
-    sa[i] = __ldcg(&gs.h[i]);
-    sb[i] = __ldcg(&gs.h[j + i]);
+  // every operand of the serial part is fetched in parallel first (one round trip)
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) {
+    if (i < j) {
+      sa[i] = __ldcg(&gs.h[i]);
+      sb[i] = __ldcg(&gs.h[j + i]);
+      scol[i] = __ldcg(&gs.Hr[(size_t)(j - 1) * LD + i]);
+    }
+    if (i + 1 < j) {
+      scs[i] = __ldcg(&gs.cs[i]);
+      ssn[i] = __ldcg(&gs.sn[i]);
+    }
   }
+  if (threadIdx.x == 32) s_nu = __ldcg(&gs.h[2 * j]);
+  if (threadIdx.x == 64 && j >= 1) s_g = __ldcg(&gs.g[j - 1]);
   __syncthreads();
   if (threadIdx.x == 0) {
-    const double nu = __ldcg(&gs.h[2 * j]);
+    const double nu = s_nu;
     double aa = 0.0;
     for (int i = 0; i < j; ++i) aa = fma(sa[i], sa[i], aa);
     const double bet2 = nu - aa;
@@ -614,16 +634,16 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
     if (j >= 1) {  // finalise column j-1 and its Givens rotation
       double* Hrc = gs.Hr + (size_t)(j - 1) * LD;
       double* Hc = gs.H + (size_t)(j - 1) * LD;
-      double col[MAX_RESTART + 1];
+      double* col = scol;
       for (int i = 0; i < j; ++i) {
-        col[i] = Hrc[i] + sa[i];
+        col[i] += sa[i];
         Hrc[i] = col[i];
       }
       col[j] = bet;
       Hrc[j] = bet;
       const int c = j - 1;
       for (int i = 0; i < c; ++i) {
-        const double ci = gs.cs[i], si = gs.sn[i];
+        const double ci = scs[i], si = ssn[i];
         const double t = ci * col[i] + si * col[i + 1];
         col[i + 1] = -si * col[i] + ci * col[i + 1];
         col[i] = t;
@@ -635,7 +655,7 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
       col[c] = den;
       col[c + 1] = 0.0;
       for (int i = 0; i <= j; ++i) Hc[i] = col[i];
-      const double gc = gs.g[c];
+      const double gc = s_g;
       gs.g[c + 1] = -sn * gc;
       gs.g[c] = cn * gc;
       s.iters += 1;
