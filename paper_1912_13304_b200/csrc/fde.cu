@@ -989,10 +989,10 @@ void build(fde_handle h, const fde_desc* d) {
     h->sine_legacy = !(sb && std::strcmp(sb, "2") == 0);
     const char* pq = std::getenv("FDE_SINE_PQ");
     h->sine_pqs = !(pq && std::strcmp(pq, "direct") == 0);
-    // concurrent body where it measured faster on the B200 (one RHS, n <= 2047;
-    // DESIGN.md §5.4); FDE_SINE_RC=1 / 0 forces it on / off
+    // concurrent body where it measured faster on the B200 (n <= 2047, any
+    // batch); FDE_SINE_RC=1 / 0 forces it on / off
     const char* rc = std::getenv("FDE_SINE_RC");
-    h->sine_rc = rc ? std::strcmp(rc, "0") != 0 : (h->batch == 1 && n <= 2047);
+    h->sine_rc = rc ? std::strcmp(rc, "0") != 0 : (n <= 2047);
     const char* go = std::getenv("FDE_GM_ORTH");
     h->gm_dcgs = !(go && std::strcmp(go, "cgs2") == 0);
     const char* gw = std::getenv("FDE_GM_WS");

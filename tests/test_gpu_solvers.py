@@ -247,7 +247,7 @@ def test_profile_abis_report_every_kernel(torch_cuda):
     assert all(us > 0 for _, us in unit)
     x = torch_cuda.zeros_like(b)
     live, stats = h.profile_solve(b, x, "pcg", 1e-10, 4)
-    assert [nm for nm, _ in live] == ["sine_op_rc", "sine_xr_rc"]   # one RHS, n <= 2047: the concurrent body
+    assert [nm for nm, _ in live] == ["sine_op_rc", "sine_xr_rc"]   # n <= 2047: the concurrent body
     assert stats[0]["iters"] == 4
     h.close()
     p = W.config(4, n=127)
