@@ -227,7 +227,9 @@ struct LaunchCfgS {
 #ifndef FDE_SINE_COL_FPC
 #define FDE_SINE_COL_FPC 2
 #endif
-  static constexpr int WANT = COL ? (128 / P > FDE_SINE_COL_FPC ? 128 / P : FDE_SINE_COL_FPC) : (128 / P > 1 ? 128 / P : 1);
+  // MODE 5 is the persistent 1D solve: one line (pair) per RHS, so one group per CTA
+  // (extra groups would only add threads to every barrier of the loop)
+  static constexpr int WANT = MODE == 5 ? 1 : (COL ? (128 / P > FDE_SINE_COL_FPC ? 128 / P : FDE_SINE_COL_FPC) : (128 / P > 1 ? 128 / P : 1));
   static constexpr int FPC0 = WANT < BY_THR ? WANT : BY_THR;
   static constexpr int FPC = FPC0 < BY_SMEM ? FPC0 : BY_SMEM;
   static constexpr int THREADS = FPC * P;
