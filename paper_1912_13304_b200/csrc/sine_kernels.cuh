@@ -152,9 +152,6 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
 #pragma unroll
       for (int c = 0; c < NV; ++c) {
         if (vec2) {
-#ifdef FDE_EXP_COL1
-          if (MODE == 7 && c == 1) { g0v[c][i] = 0.0; g1v[c][i] = 0.0; continue; }
-#endif
           const double2 pr = ok ? *reinterpret_cast<const double2*>(src[c] + o0) : make_double2(0.0, 0.0);
           g0v[c][i] = pr.x;
           g1v[c][i] = pr.y;
