@@ -17,7 +17,9 @@ import workloads as W  # noqa: E402
 from paper_1912_13304_b200 import fde  # noqa: E402
 
 fde.lib.fde_debug_probes.argtypes = [ctypes.c_void_p, ctypes.c_int64]
-p = W.config(5, n=1023)
+CFG = int(os.environ.get("PROBE_CFG", "5"))
+NN = int(os.environ.get("PROBE_N", "1023"))
+p = W.config(CFG, n=NN)
 h = fde.Fde.from_problem(p, stream=torch.cuda.current_stream().cuda_stream)
 b = torch.from_numpy(p.rhs.copy()).cuda()
 x = torch.zeros_like(b)
