@@ -1025,11 +1025,24 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
   __shared__ double tot[3];
   double sl[3] = {0.0, 0.0, 0.0};
   const double* pr = k.part + (size_t)rhs * 3 * KPMAX;
+  // only the slots this pass filled (PQ: slot 0; XR/RZ/INIT/SROW: 1, 2), 8 CTAs' worth in flight
+  const bool use0 = (k.mode & KM_PQ) != 0, use12 = (k.mode & (KM_XR | KM_RZ | KM_INIT | KM_SROW)) != 0;
+  if (use0 && !use12) {
+#pragma unroll 8
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) sl[0] += __ldcg(pr + b);
+  } else if (use12 && !use0) {
+#pragma unroll 8
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+      sl[1] += __ldcg(pr + KPMAX + b);
+      sl[2] += __ldcg(pr + 2 * KPMAX + b);
+    }
+  } else {
 #pragma unroll 4
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-    sl[0] += __ldcg(pr + b);
-    sl[1] += __ldcg(pr + KPMAX + b);
-    sl[2] += __ldcg(pr + 2 * KPMAX + b);
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+      sl[0] += __ldcg(pr + b);
+      sl[1] += __ldcg(pr + KPMAX + b);
+      sl[2] += __ldcg(pr + 2 * KPMAX + b);
+    }
   }
   for (int b = threadIdx.x; b < k.xpart; b += blockDim.x) sl[0] += __ldcg(pr + KPMAX / 2 + b);
 #pragma unroll
