@@ -38,7 +38,7 @@ import workloads as W  # noqa: E402
 
 METRIC = "preconditioned Krylov iters/sec (matvec+τ-solve), % HBM roofline, 2D n=1023"
 UNIT = "PCG iters/s"
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # SMs x FP64 FMA/clk x 2 x max clock = 37.2
+FP64_DERIVED_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # SMs x FP64 FMA/clk x 2 x max clock = 37.2
 FLUSH_BYTES = 512 << 20
 
 
@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--n", type=int, default=1023)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the n=2047 and cfg4 sub-records")
     return ap.parse_args()
 
 
@@ -64,43 +65,48 @@ def workload(args):
 
 
 # ----------------------------------------------------------------- algorithmic counts
-def unit_counts(name: str, p) -> tuple:
-    """Algorithmic (bytes, flops) per launch of one kernel of the unit
-    W = matvec + τ-solve (DESIGN.md §6 / SURVEY §8(d)): bytes = compulsory
-    fp64 I/O of the kernel, flops = standard FFT count (a real FFT of length L
-    costs 2.5·L·log2 L) plus the pointwise work."""
+def unit_alg(p) -> tuple:
+    """Algorithmic (bytes, flops) of ONE unit W = matvec + τ-solve over the
+    whole batch: bytes = the compulsory fp64 I/O
+    (read x, write y, read r, write z: 32 B/element; + fields for variable
+    coefficients: 2D +32, 1D +16; +8 for the 1/D field of TAU_D); flops = the
+    standard FFT count per line (a real FFT of length L = 2.5·L·log2 L):
+    constant-symmetric Toeplitz 10·m·log2(2m) + 2m + 2n, variable
+    15·m·log2(2m) + 12m + 5n, DST-I 2.5·m·log2(2m); 2D = both directions'
+    matvec lines + four DST passes."""
     n, m = p.n, p.n + 1
-    L = 2 * m
-    lg = np.log2(L)
-    lines = p.batch * (n if p.dims == 2 else 1)
-    el = p.batch * p.N
-    if name.startswith("toeplitz"):
-        var = name.endswith("_var")
-        col = "_cols" in name
-        b = (24 if col else 16) + (16 if var else 0)
-        f_line = (15 * m * lg + 12 * m + 5 * n) if var else (10 * m * lg + 2 * m + 2 * n)
-        return b * el, f_line * lines
-    if name.startswith("dst"):
-        return 16 * el, 2.5 * m * lg * lines + (n * lines)
-    if name.startswith("tau"):
-        return 16 * el, 2 * 2.5 * m * lg * lines + 3 * n * lines
-    if name == "copy":
-        return 16 * el, 0
-    if name.startswith("sine_op"):
-        # sine-domain operator line pass (DESIGN.md §5): DST, Toeplitz, DST on each
-        # line; rows: read r, p, write p, w; cols: read p, w, write q; 1D: read r, p,
-        # write p, q; concurrent body (rc): rows AND columns, each reading r, p_old and
-        # writing its w; the row units also write p_new and apply the lagged x += αp
-        b = {"sine_op_rows": 32, "sine_op_cols": 24, "sine_op_1d": 32, "sine_op_rc": 72}[name]
-        f_line = 2 * 2.5 * m * lg + (10 * m * lg + 2 * m + 2 * n) + 3 * n
-        return b * el, f_line * lines * (2 if name == "sine_op_rc" else 1)
-    if name == "sine_xr":
-        return 48 * el, 8 * el   # read x, p, r, q; write x, r
-    if name == "sine_xr_rc":
-        return 32 * el, 7 * el   # read r, w_r, w_c; write r (p and the lagged x are written by the row units)
-    if name.startswith("pcg_"):
-        return 48 * el, 6 * el
-    raise KeyError(name)
+    lg = np.log2(2 * m)
+    var = p.dp_field is not None
+    b_el = 32 + ((32 if p.dims == 2 else 16) if var else 0) + (8 if p.prec == W.PREC_TAU_D else 0)
+    t_line = (15 * m * lg + 12 * m + 5 * n) if var else (10 * m * lg + 2 * m + 2 * n)
+    d_line = 2.5 * m * lg
+    lines = n if p.dims == 2 else 1
+    dirs = 2 if p.dims == 2 else 1
+    flops = p.batch * lines * dirs * (t_line + 2 * d_line)
+    return b_el * p.batch * p.N, flops
+
+
+def roofline(p, us: float, peaks: dict, kernel: str, traffic) -> dict:
+    """Binding roofline of one unit's work done in `us` µs:
+    t_HBM = bytes/HBM peak, t_FP64 = flops/FP64 peak; the bound is the larger
+    of the two, frac = max(t_HBM, t_FP64)/us; both fractions are reported."""
+    by, fl = unit_alg(p)
+    t_h = by / (peaks["hbm_gbs"] * 1e9) * 1e6
+    t_f = fl / (peaks["fp64_tflops"] * 1e12) * 1e6
+    gbs = by / (us * 1e-6) / 1e9
+    tfl = fl / (us * 1e-6) / 1e12
+    hbm = {"achieved_gbs": round(gbs, 1), "peak_gbs": peaks["hbm_gbs"], "frac": round(t_h / us, 4),
+           "bytes_per_unit": int(by), "bytes_per_element": round(by / (p.batch * p.N), 2)}
+    fp = {"achieved_tflops": round(tfl, 3), "peak_tflops": round(peaks["fp64_tflops"], 3), "frac": round(t_f / us, 4),
+          "flops_per_unit": int(fl), "flops_per_element": round(fl / (p.batch * p.N), 1)}
+    if t_f >= t_h:
+        out = {"bound": "alu", "achieved": fp["achieved_tflops"], "peak": fp["peak_tflops"], "unit": "TFLOP/s",
+               "frac": fp["frac"], "peak_source": peaks["fp64_src"]}
+    else:
+        out = {"bound": "hbm", "achieved": hbm["achieved_gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+               "frac": hbm["frac"], "peak_source": peaks["hbm_src"]}
+    out.update({"traffic": traffic, "kernel": kernel, "us": round(us, 3), "hbm": hbm, "fp64": fp})
+    return out
 
 
 # ----------------------------------------------------------------- clocks
@@ -219,6 +225,72 @@ def reduce_over_ranks(ms: float, iters: int, device):
 
 
 # ----------------------------------------------------------------- product arm
+def time_solves(torch, h, p, b, x, stream, flush, steps: int, warmup: int, solver: str = "pcg"):
+    """`warmup` untimed solves, then `steps` solves each bracketed by CUDA
+    events on the handle's stream, L2 flushed before each (outside the
+    events). Returns (total ms, total iterations over all RHS)."""
+    def one():
+        if solver == "pcg":
+            return h.pcg(b, x, p.rtol, p.maxit)
+        return h.gmres(b, x, p.rtol, p.restart, p.maxit)
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    iters = 0
+    for i in range(steps):
+        flush.fill_(i & 0xff)
+        ev[i][0].record(stream)
+        st, stats = one()
+        ev[i][1].record(stream)
+        iters += sum(s_["iters"] for s_ in stats)
+        assert all(s_["converged"] for s_ in stats), stats
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(c) for a, c in ev), iters
+
+
+def live_iteration(h, p, b, torch, solver="pcg", peaks=None):
+    """Device time of every kernel of one loop body (a PCG iteration / a
+    GMRES(30) cycle) on a mid-solve state, bracketed by CUDA events on the
+    solve's stream (fde_profile_solve: warm, the solvers' own launches)."""
+    xs = torch.zeros_like(b)
+    live, _ = h.profile_solve(b, xs, solver, p.rtol, 10 if solver == "pcg" else 30, restart=p.restart)
+    tot = sum(t for _, t in live)
+    agg = {}
+    for name, us in live:
+        agg[name] = agg.get(name, 0.0) + us
+    return live, tot, agg
+
+
+def sub_record(torch, fde, args, cfg: int, n: int, solver: str, dev, stream, flush, peaks, steps=3, warmup=2):
+    """A second driver-timed workload on the same JSON line:
+    the same solve contract (device-timed, L2 flushed) plus its loop body's
+    kernels and the dominant kernel's binding roofline."""
+    p = W.config(cfg, n=n)
+    h = fde.Fde.from_problem(p, stream=stream.cuda_stream)
+    b = torch.from_numpy(p.rhs.copy()).to(dev)
+    x = torch.zeros_like(b)
+    ms, iters = time_solves(torch, h, p, b, x, stream, flush, steps, warmup, solver)
+    live, tot, agg = live_iteration(h, p, b, torch, solver)
+    rec = {"workload": "BASELINE cfg%d, n=%d (N=%d), %s" % (cfg, n, p.N,
+                                                          "PCG + tau(F) to 1e-10" if solver == "pcg"
+                                                          else "GMRES(30) right-prec. mean-coef tau to 1e-10"),
+           "value": iters / (ms / 1e3), "unit": "PCG iters/s" if solver == "pcg" else "GMRES iters/s",
+           "ms_per_step": ms / steps, "iters_per_solve": iters / steps, "steps": steps, "warmup": warmup,
+           "us_per_iter": round(ms * 1e3 / max(iters, 1), 3),
+           "loop_body_kernels_us": {k: round(v, 2) for k, v in agg.items()}}
+    if solver == "pcg":
+        top = max(live, key=lambda kv: kv[1])
+        rec["roofline"] = roofline(p, top[1], peaks, top[0], TRAFFIC.get(top[0]))
+        rec["roofline_iteration"] = roofline(p, tot, peaks, "one PCG iteration", None)
+    else:
+        # one GMRES(30) cycle applies the unit (matvec + tau-solve) once per Arnoldi step
+        steps_in_cycle = p.restart
+        rec["roofline_step"] = roofline(p, tot / steps_in_cycle, peaks, "one Arnoldi step (cycle/30)", None)
+    h.close()
+    return rec
+
+
 def run_fde(args, rank, world, local_rank):
     import torch
     from paper_1912_13304_b200 import fde
@@ -231,12 +303,10 @@ def run_fde(args, rank, world, local_rank):
     b = torch.from_numpy(p.rhs.copy()).to(dev)
     x = torch.zeros_like(b)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
-
-    def step():
-        return h.pcg(b, x, p.rtol, p.maxit)
+    peaks = measured_peaks(fde)
 
     for _ in range(args.warmup):
-        step()
+        h.pcg(b, x, p.rtol, p.maxit)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -246,19 +316,9 @@ def run_fde(args, rank, world, local_rank):
     clk.start()
     time.sleep(0.2)
     l0 = h.kernel_launches()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    iters = 0
-    for i in range(args.steps):
-        flush.fill_(i & 0xff)
-        ev[i][0].record(stream)
-        st, stats = step()
-        ev[i][1].record(stream)
-        iters += sum(s["iters"] for s in stats)
-        assert all(s["converged"] for s in stats), stats
-    torch.cuda.synchronize()
+    ms, iters = time_solves(torch, h, p, b, x, stream, flush, args.steps, 0)
     launches = h.kernel_launches() - l0
     clocks = clk.stop()
-    ms = sum(a.elapsed_time(c) for a, c in ev)
     if world > 1:
         ms, iters = reduce_over_ranks(ms, iters, dev)
     value = iters / (ms / 1e3)
@@ -278,85 +338,93 @@ def run_fde(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms += e0.elapsed_time(e1)
-        e_it += sum(s["iters"] for s in stats)
+        e_it += sum(s_["iters"] for s_ in stats)
     if world > 1:
         e_ms, e_it = reduce_over_ranks(e_ms, e_it, dev)
     e2e = {"value": e_it / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(bn.nbytes),
            "d2h_bytes_per_step": int(xn.nbytes), "path": "fde_pcg with pinned host b, x (library-staged copies)"}
 
-    # roofline: per-kernel device time of one unit W (matvec + τ-solve), L2 flushed before every launch
+    # roofline: the dominant kernel of one PCG iteration timed live
+    # (CUDA events on the solve's stream, warm), against the unit's ALGORITHMIC
+    # bytes (32 B/element) and flops (standard FFT count); binding = max
+    live, iter_us, agg = live_iteration(h, p, b, torch)
+    top_name, top_us = max(live, key=lambda kv: kv[1])
+    roof = roofline(p, top_us, peaks, top_name, TRAFFIC.get(top_name))
+    roof["share_of_iteration"] = round(top_us / iter_us, 4)
+    roof["per_iteration"] = roofline(p, iter_us, peaks, "one PCG iteration (all kernels)", None)
+    iteration = {"us_kernels": round(iter_us, 3), "us_per_iter_timed": round(ms * 1e3 / max(iters, 1) * world, 3),
+                 "kernels": [{"name": nm, "us": round(us, 3), "share": round(us / iter_us, 4)} for nm, us in live],
+                 "mode": "one PCG iteration on a mid-solve state (after 10), kernels bracketed by CUDA events, warm"}
+    # the unit W = fde_matvec + fde_tau_apply (the standard-basis operations of the ABI):
+    # warm = back-to-back launches, cold = L2 flushed before every launch
     y = torch.empty_like(b)
     z = torch.empty_like(b)
-    # live: device time of every kernel of the last PCG iteration of a solve, from
-    # CUDA event nodes captured into the solve's loop-body graph (warm, exactly
-    # the kernels and launch configuration of the timed region)
-    xs = torch.zeros_like(b)
-    live, _ = h.profile_solve(b, xs, "pcg", p.rtol, 10)
-    iter_us = sum(t for _, t in live)
-    kern = []
-    for name, us in live:
-        by, fl = unit_counts(name, p)
-        t_h = by / (MEASURED["hbm_gbs"] * 1e9) * 1e6
-        t_f = fl / (FP64_PEAK_TFLOPS * 1e12) * 1e6
-        kern.append({"name": name, "us": round(us, 3), "share": round(us / iter_us, 4), "bytes": int(by),
-                     "flops": int(fl), "hbm_frac": round(t_h / us, 4), "fp64_frac": round(t_f / us, 4)})
-    iteration = {"us_kernels": round(iter_us, 3), "us_per_iter_timed": round(ms * 1e3 / max(iters, 1) * world, 3),
-                 "kernels": kern, "mode": "one PCG iteration on a mid-solve state (after 10), kernels bracketed by CUDA events, warm"}
-    # the unit W = fde_matvec + fde_tau_apply (the standard-domain operations of the ABI):
-    # warm = back-to-back launches, cold = L2 flushed before every launch
     prof = h.profile_unit(b, y, z, reps=20, flush=None)
     prof_cold = h.profile_unit(b, y, z, reps=10, flush=flush)
     unit_us = sum(t for _, t in prof)
-    ukern = []
-    for name, us in prof:
-        by, fl = unit_counts(name, p)
-        t_h = by / (MEASURED["hbm_gbs"] * 1e9) * 1e6
-        t_f = fl / (FP64_PEAK_TFLOPS * 1e12) * 1e6
-        ukern.append({"name": name, "us": round(us, 3), "share": round(us / unit_us, 4), "bytes": int(by),
-                      "flops": int(fl), "hbm_frac": round(t_h / us, 4), "fp64_frac": round(t_f / us, 4)})
-    top = max(kern, key=lambda k: k["us"])
-    hbm_gbs = top["bytes"] / (top["us"] * 1e-6) / 1e9
-    tfl = top["flops"] / (top["us"] * 1e-6) / 1e12
-    if top["fp64_frac"] >= top["hbm_frac"]:
-        roof = {"bound": "alu", "achieved": round(tfl, 3), "peak": round(FP64_PEAK_TFLOPS, 2), "unit": "TFLOP/s",
-                "frac": round(tfl / FP64_PEAK_TFLOPS, 4),
-                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6)"}
-    else:
-        roof = {"bound": "hbm", "achieved": round(hbm_gbs, 1), "peak": MEASURED["hbm_gbs"], "unit": "GB/s",
-                "frac": round(hbm_gbs / MEASURED["hbm_gbs"], 4), "peak_source": MEASURED["src"]}
-    roof.update({"kernel": top["name"], "traffic": TRAFFIC.get(top["name"]),
-                 "hbm": {"achieved_gbs": round(hbm_gbs, 1), "frac": round(hbm_gbs / MEASURED["hbm_gbs"], 4)},
-                 "fp64": {"achieved_tflops": round(tfl, 3), "frac": round(tfl / FP64_PEAK_TFLOPS, 4)}})
-    unit_bytes = sum(k["bytes"] for k in ukern)
-    unit_flops = sum(k["flops"] for k in ukern)
-    unit_roof = max(unit_bytes / (MEASURED["hbm_gbs"] * 1e9), unit_flops / (FP64_PEAK_TFLOPS * 1e12)) * 1e6
-    unit = {"us": round(unit_us, 3), "kernels": ukern, "mode": "warm L2 (back-to-back launches)",
+    unit = {"us": round(unit_us, 3), "kernels": {nm: round(us, 3) for nm, us in prof},
+            "mode": "warm L2 (back-to-back launches)",
             "cold_us": {nm: round(us, 3) for nm, us in prof_cold}, "cold_total_us": round(sum(t for _, t in prof_cold), 3),
-            "hbm_frac": round(unit_bytes / (MEASURED["hbm_gbs"] * 1e9) * 1e6 / unit_us, 4),
-            "binding_roofline_frac": round(unit_roof / unit_us, 4)}
+            "roofline": roofline(p, unit_us, peaks, "fde_matvec + fde_tau_apply (warm)", None)}
+    h.close()
+
+    extra = {}
+    if not args.no_sub and rank == 0:
+        extra["n2047"] = sub_record(torch, fde, args, 5, 2047, "pcg", dev, stream, flush, peaks)
+        extra["cfg4"] = sub_record(torch, fde, args, 4, 1023, "gmres", dev, stream, flush, peaks, steps=2, warmup=1)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": desc,
            "iters_per_solve": iters / (args.steps * world), "clocks": clocks, "e2e": e2e,
-           "gpu_launches": int(launches), "roofline": roof, "iteration": iteration, "unit_w": unit}
+           "gpu_launches": int(launches), "roofline": roof, "iteration": iteration, "unit_w": unit,
+           "peaks": {k: v for k, v in peaks.items()}}
+    out.update(extra)
     if rank == 0 and not args.no_cpu_baseline:
-        it = 40
-        dt, k, thr = oracle_pcg_sample(p, it)
-        out["cpu_baseline"] = {"value": k / dt, "unit": UNIT, "cores": thr, "kind": "oracle",
-                               "sample": "%d PCG iterations of the same system (RHS 0) by the dense fp64 oracle" % k,
-                               "cpu": cpu_model(), "seconds": round(dt, 2)}
-    h.close()
+        out["cpu_baseline"] = cpu_baseline(p)
     return out
 
 
-def measured_peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+def cpu_baseline(p) -> dict:
+    """The oracle (dense fp64 CPU, as it stands) on a bounded sample of the
+    same workload: PCG iterations of the same system on RHS 0, with all host
+    cores (BLAS threads = os.cpu_count()) and with one thread."""
+    ncpu = os.cpu_count() or 1
     try:
-        d = json.load(open(path))
-        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    dt, k, thr = oracle_pcg_sample(p, 40)
+    rec = {"value": k / dt, "unit": UNIT, "cores": thr, "os_cpu_count": ncpu, "kind": "oracle",
+           "sample": "%d PCG iterations of the same system (RHS 0) by the dense fp64 oracle, %d BLAS threads"
+                     % (k, thr), "cpu": cpu_model(), "seconds": round(dt, 2)}
+    if threadpool_limits is not None:
+        with threadpool_limits(limits=1):
+            dt1, k1, _ = oracle_pcg_sample(p, 3)
+        rec["single_thread"] = {"value": k1 / dt1, "unit": UNIT, "cores": 1, "seconds": round(dt1, 2),
+                                "sample": "%d PCG iterations, BLAS limited to 1 thread" % k1}
+    return rec
+
+
+def measured_peaks(fde=None):
+    """Roofline denominators: HBM = MEASURED_PEAKS.json (driver-measured copy
+    bandwidth); FP64 = measured on this GPU by fde_measure_fp64_peak (DFMA
+    chains over every SM), else the derived 148 SMs x 64 FMA/clk x 2 x 1.965 GHz."""
+    out = {}
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        out.update(hbm_gbs=float(d["hbm_gbs"]), hbm_src="MEASURED_PEAKS.json hbm_gbs (measured copy)")
     except Exception:
-        return {"hbm_gbs": 6650.0, "src": "fallback 6.65 TB/s (B200_PROFILING.md)"}
+        out.update(hbm_gbs=6650.0, hbm_src="fallback 6.65 TB/s (B200_PROFILING.md)")
+    out.update(fp64_tflops=FP64_DERIVED_TFLOPS, fp64_src="derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz")
+    if fde is not None:
+        try:
+            v = fde.measure_fp64_peak(5)
+            if v > 1.0:
+                out.update(fp64_tflops=v, fp64_src="measured on this GPU: fde_measure_fp64_peak (DFMA chains, best of 5)")
+        except Exception as e:  # pragma: no cover
+            out["fp64_err"] = str(e)
+    return out
 
 
 def ncu_traffic():
@@ -369,7 +437,6 @@ def ncu_traffic():
         return {}
 
 
-MEASURED = measured_peaks()
 TRAFFIC = ncu_traffic()
 
 

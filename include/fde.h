@@ -151,6 +151,14 @@ fde_status fde_profile_unit(fde_handle h, const double* x, double* y, double* z,
                             int64_t flush_bytes, int32_t max_kernels, int32_t* count, double* us,
                             const char** names);
 
+/* Measurement support (bench.py's roofline denominator): the FP64 FMA
+ * throughput of the CURRENT device, measured by a kernel of independent DFMA
+ * chains over every SM (`reps` timed launches, best one; CUDA events on an
+ * internal stream). *tflops receives 2 x DFMA lanes per second / 1e12.
+ * Status FDE_ERR_INVALID_ARG for a NULL output or reps < 1, FDE_ERR_CUDA on a
+ * CUDA failure. Synchronises the device's internal stream. */
+fde_status fde_measure_fp64_peak(int32_t reps, double* tflops);
+
 /* Measurement support: run a solve (solver 0 = fde_pcg, 1 = fde_gmres right-
  * preconditioned with `restart`) for at most `maxit` iterations, then run ONE
  * more loop body (a PCG iteration / a GMRES cycle) on that mid-solve state

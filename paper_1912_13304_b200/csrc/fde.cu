@@ -302,8 +302,11 @@ struct fde_handle_s {
   int g_pcg_chunk = 0, g_pcg_nodes = 0;
   cudaGraphExec_t g_gm = nullptr;
   int g_gm_restart = 0, g_gm_left = -1, g_gm_nodes = 0;
-  double g_rtol = -1.0;
-  int g_maxit = -1;
+  // rtol and maxit are baked into each captured graph (kernel parameters and
+  // the WHILE node's loop bound), so every graph carries its own key
+  double g_pcg_rtol = -1.0, g_gm_rtol = -1.0;
+  int g_pcg_maxit = -1, g_gm_maxit = -1;
+  int g_pcg_kind = -1;              // 0 = standard-basis body, 1 = sine-domain body
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
   bool gm_dcgs = true;              // GMRES orthogonalisation by DCGS2 (FDE_GM_ORTH=cgs2: classical CGS2)
@@ -409,11 +412,9 @@ int launch_sineop_k(fde_handle h, const LineArgs& a0) {
   a.twp = h->twps_t;
   a.pitch = h->sine_pitch;
   auto kern = k_sineop_lines<KM, COL, C::FPC, MODE>;
-  static bool attr = false;
-  if (!attr) {
-    FDE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr = true;
-  }
+  // per launch (a host-side attribute of the current device; captured launches
+  // pay it once): a process may drive handles on several devices
+  FDE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   const int npairs = (a.nlines + 1) / 2;
   const dim3 grid((npairs + C::FPC - 1) / C::FPC, h->batch);
   launch_named(h, (MODE == 0 || MODE == 3) ? "sine_op_rows" : ((MODE == 1 || MODE == 4) ? "sine_op_cols" : "sine_op_1d"),
@@ -431,11 +432,9 @@ void launch_sineop_rc_k(fde_handle h, const LineArgs& ar0, const LineArgs& ac0) 
     a->pitch = h->sine_pitch;
   }
   auto kern = k_sineop_rc<KM, C::FPC>;
-  static bool attr = false;
-  if (!attr) {
-    FDE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr = true;
-  }
+  // per launch (a host-side attribute of the current device; captured launches
+  // pay it once): a process may drive handles on several devices
+  FDE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   const int gr = ((ar.nlines + 1) / 2 + C::FPC - 1) / C::FPC;
   const int gc = ((ac.nlines + 1) / 2 + C::FPC - 1) / C::FPC;
   if (gr + gc > KPMAX) throw FdeFail{FDE_ERR_UNSUPPORTED, "concurrent sine body grid exceeds the partial slots"};
@@ -1433,11 +1432,12 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
     a.kf.mode = KM_GATE;
     a.persist = 1;
     FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 5>(h, a)));
-  } else if (!h->no_graph && (!h->g_pcg || h->g_rtol != rtol || h->g_maxit != maxit)) {
+  } else if (!h->no_graph && (!h->g_pcg || h->g_pcg_kind != 1 || h->g_pcg_rtol != rtol || h->g_pcg_maxit != maxit)) {
     if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
     h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { sine_iteration(h, rtol, maxit); });
-    h->g_rtol = rtol;
-    h->g_maxit = maxit;
+    h->g_pcg_kind = 1;
+    h->g_pcg_rtol = rtol;
+    h->g_pcg_maxit = maxit;
   }
   if (persist1d) {
   } else if (h->no_graph) {  // FDE_GRAPH=0 (profilers): the same loop body from the host
@@ -1489,11 +1489,12 @@ fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int ma
 
   // the whole iteration loop is ONE graph launch: a conditional WHILE node
   // whose body is one PCG iteration plus k_loop_ctrl (no host round trips)
-  if (!h->g_pcg || h->g_rtol != rtol || h->g_maxit != maxit) {
+  if (!h->g_pcg || h->g_pcg_kind != 0 || h->g_pcg_rtol != rtol || h->g_pcg_maxit != maxit) {
     if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
     h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { pcg_iteration(h, va); });
-    h->g_rtol = rtol;
-    h->g_maxit = maxit;
+    h->g_pcg_kind = 0;
+    h->g_pcg_rtol = rtol;
+    h->g_pcg_maxit = maxit;
   }
   FDE_CUDA(cudaGraphLaunch(h->g_pcg, h->st));
   if (is_device_ptr(x)) {
@@ -1625,14 +1626,14 @@ fde_status run_gmres(fde_handle h, const double* b, double* x, double rtol, int 
 
   // one graph launch per solve: WHILE(some RHS unfinished) { one restart cycle }
   const int max_cycles = maxit / restart + 2;
-  if (!h->no_graph && (!h->g_gm || h->g_gm_restart != restart || h->g_gm_left != left || h->g_rtol != rtol ||
-                      h->g_maxit != maxit)) {
+  if (!h->no_graph && (!h->g_gm || h->g_gm_restart != restart || h->g_gm_left != left || h->g_gm_rtol != rtol ||
+                      h->g_gm_maxit != maxit)) {
     if (h->g_gm) { cudaGraphExecDestroy(h->g_gm); h->g_gm = nullptr; }
     h->g_gm_nodes = build_while_graph(h, &h->g_gm, max_cycles, [&] { gmres_cycle(h, va, restart, left); });
     h->g_gm_restart = restart;
     h->g_gm_left = left;
-    h->g_rtol = rtol;
-    h->g_maxit = maxit;
+    h->g_gm_rtol = rtol;
+    h->g_gm_maxit = maxit;
   }
   if (h->no_graph) {  // FDE_GRAPH=0 (profilers): the same cycle from the host
     for (int c = 0; c < max_cycles; ++c) {
@@ -1650,6 +1651,26 @@ fde_status run_gmres(fde_handle h, const double* b, double* x, double rtol, int 
   const fde_status ws = worst_status(h, st, false);
   if (!h->no_graph) h->launches += (long long)read_loops(h) * h->g_gm_nodes;
   return ws;
+}
+
+
+// FP64 FMA throughput probe (fde_measure_fp64_peak): 16 independent DFMA
+// chains per thread, enough resident warps per SM to cover the DFMA latency
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+  double x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = threadIdx.x * 1e-9 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = fma(x[k], a, b);
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;
 }
 
 void free_handle(fde_handle h) {
@@ -1789,6 +1810,47 @@ const char* fde_status_str(fde_status s) {
 const char* fde_last_error(fde_handle h) { return h ? h->err.c_str() : "NULL handle"; }
 
 int64_t fde_kernel_launches(fde_handle h) { return h ? (int64_t)h->launches : 0; }
+
+fde_status fde_measure_fp64_peak(int32_t reps, double* tflops) {
+  if (!tflops || reps < 1) return FDE_ERR_INVALID_ARG;
+  cudaStream_t st = nullptr;
+  cudaEvent_t a = nullptr, b = nullptr;
+  double* out = nullptr;
+  fde_status rs = FDE_OK;
+  try {
+    int dev = 0, sms = 0;
+    FDE_CUDA(cudaGetDevice(&dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FDE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    FDE_CUDA(cudaEventCreate(&a));
+    FDE_CUDA(cudaEventCreate(&b));
+    FDE_CUDA(cudaMalloc(&out, sizeof(double)));
+    const int blocks = sms * 8, threads = 256, iters = 2048;
+    k_dfma_peak<<<blocks, threads, 0, st>>>(out, 64, 0.999999, 1e-7);  // warm-up
+    FDE_CUDA(cudaGetLastError());
+    float best = 1e30f;
+    for (int r = 0; r < reps; ++r) {
+      FDE_CUDA(cudaEventRecord(a, st));
+      k_dfma_peak<<<blocks, threads, 0, st>>>(out, iters, 0.999999, 1e-7);
+      FDE_CUDA(cudaEventRecord(b, st));
+      FDE_CUDA(cudaEventSynchronize(b));
+      float ms = 0.f;
+      FDE_CUDA(cudaEventElapsedTime(&ms, a, b));
+      best = std::min(best, ms);
+    }
+    const double lanes = (double)blocks * threads * iters * 8 * 16;
+    *tflops = 2.0 * lanes / (best * 1e-3) / 1e12;
+  } catch (const FdeFail& f) {
+    rs = f.s;
+  } catch (...) {
+    rs = FDE_ERR_CUDA;
+  }
+  if (out) cudaFree(out);
+  if (a) cudaEventDestroy(a);
+  if (b) cudaEventDestroy(b);
+  if (st) cudaStreamDestroy(st);
+  return rs;
+}
 
 #ifdef FDE_PROBES
 // tools/phase_probe.py: copy the probe array out ([8][2048][8] u64) and reset the slot counter

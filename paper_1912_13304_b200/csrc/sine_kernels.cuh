@@ -453,11 +453,22 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
   if (MODE == 5) {  // α_k = ρ_k / (p̂·q̂) inside the CTA
     acc[1] = acc[2] = 0.0;
     block_reduce3(acc, scr);
+    __shared__ int s_stop5;
     if (threadIdx.x == 0) {
       SolveState& s = *sst;
-      if (!(acc[0] > 0.0)) { s.status = isfinite(acc[0]) ? ST_NOT_SPD : ST_NONFINITE; finish_rhs(a.kf.ctr, s); }
-      else s.alpha = s.rho / acc[0];
+      if (!(acc[0] > 0.0)) {
+        // breakdown: no pending update (α = 0) and no further body, so the
+        // status, iters and rnorm of this body stand
+        s.status = isfinite(acc[0]) ? ST_NOT_SPD : ST_NONFINITE;
+        s.alpha = 0.0;
+        finish_rhs(a.kf.ctr, s);
+      } else {
+        s.alpha = s.rho / acc[0];
+      }
+      s_stop5 = !s.cyc_active;
     }
+    __syncthreads();
+    if (s_stop5) break;
   } else if (MODE == 0 && (a.kf.mode & KM_PQX)) {  // the row pass's share of p̂·q̂, finalised by the column pass
     block_reduce3(acc, scr);
     if (threadIdx.x == 0) a.kf.part[(size_t)blockIdx.y * 3 * KPMAX + KPMAX / 2 + blockIdx.x] = acc[0];

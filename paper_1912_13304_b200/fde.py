@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 from typing import Optional
 
 import numpy as np
@@ -85,6 +86,17 @@ lib.fde_profile_solve.argtypes = [_H, _P, _P, ctypes.c_double, ctypes.c_int32, c
                                   ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(fde_stats)]
 lib.fde_profile_solve.restype = ctypes.c_int
+lib.fde_measure_fp64_peak.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
+lib.fde_measure_fp64_peak.restype = ctypes.c_int
+
+
+def measure_fp64_peak(reps: int = 5) -> float:
+    """fde_measure_fp64_peak: DFMA throughput of the current device, TFLOP/s."""
+    v = ctypes.c_double(0.0)
+    st = lib.fde_measure_fp64_peak(int(reps), ctypes.byref(v))
+    if st != FDE_OK:
+        raise FdeError(st, "fde_measure_fp64_peak")
+    return v.value
 
 
 def fde_status_str(s: int) -> str:
@@ -97,27 +109,37 @@ class FdeError(RuntimeError):
         self.status = status
 
 
-def _ptr(a) -> int:
-    """Raw pointer of a float64 C-contiguous torch tensor or numpy array."""
+def _ptr(a, numel: Optional[int] = None, device: Optional[int] = None) -> int:
+    """Raw pointer of a float64 C-contiguous torch tensor or numpy array.
+    With `numel`, the array must hold exactly that many elements (the library
+    reads/writes batch·N values behind the pointer); with `device`, a CUDA
+    tensor must live on that device (the handle's)."""
     if isinstance(a, np.ndarray):
         if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
             raise TypeError("numpy arrays must be C-contiguous float64")
+        if numel is not None and a.size != numel:
+            raise ValueError("array has %d elements, the handle needs batch*N = %d" % (a.size, numel))
         return a.ctypes.data
     # torch tensor (imported lazily: torch is plumbing, not a dependency of the binding)
     if getattr(a, "dtype", None) is None or str(a.dtype) != "torch.float64":
         raise TypeError("tensors must be float64")
     if not a.is_contiguous():
         raise TypeError("tensors must be contiguous")
+    if numel is not None and a.numel() != numel:
+        raise ValueError("tensor has %d elements, the handle needs batch*N = %d" % (a.numel(), numel))
+    if device is not None and a.is_cuda and a.device.index != device:
+        raise ValueError("tensor is on cuda:%d, the handle on cuda:%d" % (a.device.index, device))
     return a.data_ptr()
 
 
-def _field(v):
+def _field(v, N: int):
+    """A coefficient field (length N, copied by fde_create)."""
     if v is None:
         return None, None
     if isinstance(v, np.ndarray):
         v = np.ascontiguousarray(v, dtype=np.float64)
-        return v, v.ctypes.data
-    return v, _ptr(v)
+        return v, _ptr(v, N)
+    return v, _ptr(v, N)
 
 
 class Fde:
@@ -134,7 +156,7 @@ class Fde:
         d.dp, d.dm, d.ep, d.em = dp, dm, ep, em
         keep = []
         for name, v in (("dp_field", dp_field), ("dm_field", dm_field), ("ep_field", ep_field), ("em_field", em_field)):
-            obj, p = _field(v)
+            obj, p = _field(v, n ** dims)
             keep.append(obj)
             setattr(d, name, p)
         d.prec, d.cx, d.cy, d.ywt = prec, cx, cy, ywt
@@ -142,6 +164,12 @@ class Fde:
         self.desc = d
         self.n, self.dims, self.batch = n, dims, batch
         self.N = n ** dims
+        self.numel = batch * self.N
+        # the library creates the handle on the calling thread's current device
+        self.device = None
+        torch = sys.modules.get("torch")
+        if torch is not None and torch.cuda.is_available():
+            self.device = torch.cuda.current_device()
         self._h = _H()
         st = lib.fde_create(ctypes.byref(d), ctypes.byref(self._h))
         if st != FDE_OK:
@@ -154,26 +182,30 @@ class Fde:
                    p.dp_field, p.dm_field, p.ep_field, p.em_field, p.prec, p.cx, p.cy, 1.0,
                    p.batch, p.stencil, stream)
 
+    def _v(self, a) -> int:
+        """Pointer of a length batch·N vector argument (size and device checked)."""
+        return _ptr(a, self.numel, self.device)
+
     def _check(self, st):
         if st != FDE_OK and st != FDE_ERR_NOT_CONVERGED:
             raise FdeError(st, lib.fde_last_error(self._h).decode())
         return st
 
     def matvec(self, x, y):
-        return self._check(lib.fde_matvec(self._h, _ptr(x), _ptr(y)))
+        return self._check(lib.fde_matvec(self._h, self._v(x), self._v(y)))
 
     def tau_apply(self, r, z):
-        return self._check(lib.fde_tau_apply(self._h, _ptr(r), _ptr(z)))
+        return self._check(lib.fde_tau_apply(self._h, self._v(r), self._v(z)))
 
     def pcg(self, b, x, rtol: float = 1e-10, maxit: int = 5000):
         stats = (fde_stats * self.batch)()
-        st = self._check(lib.fde_pcg(self._h, _ptr(b), _ptr(x), rtol, maxit, stats))
+        st = self._check(lib.fde_pcg(self._h, self._v(b), self._v(x), rtol, maxit, stats))
         return st, [dict(iters=s.iters, restarts=s.restarts, converged=bool(s.converged), status=s.status,
                          rel_res=s.rel_res) for s in stats]
 
     def gmres(self, b, x, rtol: float = 1e-10, restart: int = 30, maxit: int = 20000, left: bool = False):
         stats = (fde_stats * self.batch)()
-        st = self._check(lib.fde_gmres(self._h, _ptr(b), _ptr(x), rtol, restart, maxit, int(left), stats))
+        st = self._check(lib.fde_gmres(self._h, self._v(b), self._v(x), rtol, restart, maxit, int(left), stats))
         return st, [dict(iters=s.iters, restarts=s.restarts, converged=bool(s.converged), status=s.status,
                          rel_res=s.rel_res) for s in stats]
 
@@ -191,7 +223,7 @@ class Fde:
         cnt = ctypes.c_int32(0)
         fp = 0 if flush is None else flush.data_ptr()
         fb = 0 if flush is None else flush.numel() * flush.element_size()
-        self._check(lib.fde_profile_unit(self._h, _ptr(x), _ptr(y), _ptr(z), reps, fp or None, fb, MAXK,
+        self._check(lib.fde_profile_unit(self._h, self._v(x), self._v(y), self._v(z), reps, fp or None, fb, MAXK,
                                          ctypes.byref(cnt), us, names))
         return [(names[i].decode(), us[i]) for i in range(min(cnt.value, MAXK))]
 
@@ -203,7 +235,7 @@ class Fde:
         names = (ctypes.c_char_p * MAXK)()
         cnt = ctypes.c_int32(0)
         stats = (fde_stats * self.batch)()
-        self._check(lib.fde_profile_solve(self._h, _ptr(b), _ptr(x), rtol, maxit, 0 if solver == "pcg" else 1,
+        self._check(lib.fde_profile_solve(self._h, self._v(b), self._v(x), rtol, maxit, 0 if solver == "pcg" else 1,
                                           restart, MAXK, ctypes.byref(cnt), us, names, stats))
         return ([(names[i].decode(), us[i]) for i in range(min(cnt.value, MAXK))],
                 [dict(iters=s.iters, converged=bool(s.converged)) for s in stats])

@@ -85,3 +85,10 @@ def test_binding_rejects_bad_arrays():
         fde._ptr(np.zeros(4, dtype=np.float32))
     with pytest.raises(TypeError):
         fde._ptr(np.zeros((4, 4))[:, 1])
+    # the library reads/writes batch·N elements behind every vector pointer:
+    # a short (or long) array is refused before any call into libfde
+    with pytest.raises(ValueError):
+        fde._ptr(np.zeros(10), numel=11)
+    with pytest.raises(ValueError):
+        fde._ptr(np.zeros((2, 6)), numel=11)
+    assert fde._ptr(np.zeros((1, 11)), numel=11) != 0

@@ -428,3 +428,61 @@ def test_table2_ptri_iterations(row):
     ex = W.example1(alpha, n1 - 1)
     it, _ = O.example1_run(ex, alpha, n1 - 1, O.PREC_TRI)
     assert abs(it - row[2]) <= 0.15, it
+
+
+# ------------------------------------------------ TAU_DSYM (Eq. prop_1D) ---
+
+@pytest.mark.parametrize("dims,d", [(1, 2.7), (2, 0.35)])
+def test_tau_dsym_constant_D_on_sine_modes(dims, d):
+    """Eq. prop_1D (2D P:L380): P = D^{1/2} τ(F) D^{1/2}. With
+    d₊ = d₋ (= e₊ = e₋) = d constant, D = d·I, so P = d·τ(F) and every sine
+    mode (an eigenvector of τ(F)) satisfies P⁻¹ v = v / (d·F(θ)).
+    The expected value uses the mode built from sin(·) and the symbol from its
+    closed form (both pinned above), not the oracle's preconditioner code. A
+    plausible slip (D⁻¹ or D^{+1/2} in place of D^{-1/2}, one-sided scaling)
+    changes the factor d."""
+    n = 15
+    s = O.System(dims, n, 1.3, 1.7, 0.2, d, d, d, d)
+    cx, cy = 0.9, 1.4
+    th = O.theta_grid(n)
+    for (i, j) in ((1, 1), (4, 9), (15, 2)):
+        if dims == 1:
+            v = O.sine_mode(n, i)
+            F = cx * O.symbol_p(1.3, th[i - 1])
+        else:
+            v = O.sine_mode(n, i, j)
+            F = cx * O.symbol_p(1.3, th[i - 1]) + cy * O.symbol_p(1.7, th[j - 1])
+        z = s.prec_solve(v, O.PREC_TAU_DSYM, cx, cy)
+        assert np.allclose(z, v / (d * F), rtol=0, atol=1e-13 * np.abs(v / (d * F)).max())
+
+
+def test_tau_dsym_is_spd_and_similar_to_tau_d():
+    """With a variable D: P_DSYM⁻¹ = D^{-1/2} τ⁻¹ D^{-1/2} is symmetric positive
+    definite (τ(F) is SPD: F > 0 on the grid and S is orthogonal), and
+    it is similar to the as-measured P_F⁻¹ = D⁻¹ τ⁻¹ (R6, pinned by Table 1's
+    κ to 12/12 cells): D^{1/2} P_F⁻¹ D^{-1/2} = P_DSYM⁻¹. Matrices are built
+    column by column from prec_solve on unit vectors."""
+    rng = np.random.default_rng(11)
+    n = 24
+    s = O.System(1, n, 1.6, 0, 0.05, 0.5 + rng.random(n), 0.5 + rng.random(n))
+    E = np.eye(n)
+    Psym = np.column_stack([s.prec_solve(E[k], O.PREC_TAU_DSYM) for k in range(n)])
+    Pd = np.column_stack([s.prec_solve(E[k], O.PREC_TAU_D) for k in range(n)])
+    assert np.abs(Psym - Psym.T).max() <= 1e-13 * np.abs(Psym).max()
+    assert np.linalg.eigvalsh(0.5 * (Psym + Psym.T)).min() > 0
+    assert np.abs(Pd - Pd.T).max() > 1e-3 * np.abs(Pd).max()      # the as-measured kind is not symmetric
+    h = np.sqrt(s.D())
+    assert np.allclose(h[:, None] * Pd / h[None, :], Psym, rtol=0, atol=1e-13 * np.abs(Psym).max())
+
+
+@pytest.mark.parametrize("n1,kappa", [(64, 30.9), (128, 63.8), (256, 132.3)])
+def test_tau_dsym_kappa_survey_values(n1, kappa):
+    """κ₂(P_DSYM⁻¹ M) on Example 1 at α = 1.2: SURVEY Appendix A
+    lists 30.9/63.8/132.3/274.8 for n1+1 = 64..512 (SURVEY-DERIVED values from
+    the survey's own scratch computation, not printed in the paper; the paper's
+    Table 1 matches the τ·D reading instead, 30.8/63.7/132.2/274.7)."""
+    alpha, n = 1.2, n1 - 1
+    ex = W.example1(alpha, n)
+    s = O.example1_matrices(ex, alpha, n)
+    M = s.dense()
+    assert round(O.cond2(np.linalg.solve(s.prec_dense(O.PREC_TAU_DSYM), M)), 1) == kappa
