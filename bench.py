@@ -281,7 +281,7 @@ def sub_record(torch, fde, args, cfg: int, n: int, solver: str, dev, stream, flu
            "loop_body_kernels_us": {k: round(v, 2) for k, v in agg.items()}}
     if solver == "pcg":
         top = max(live, key=lambda kv: kv[1])
-        rec["roofline"] = roofline(p, top[1], peaks, top[0], TRAFFIC.get(top[0]))
+        rec["roofline"] = roofline(p, top[1], peaks, top[0], TRAFFIC.get("%s@%d" % (top[0], n)))
         rec["roofline_iteration"] = roofline(p, tot, peaks, "one PCG iteration", None)
     else:
         # one GMRES(30) cycle applies the unit (matvec + tau-solve) once per Arnoldi step
@@ -349,7 +349,7 @@ def run_fde(args, rank, world, local_rank):
     # bytes (32 B/element) and flops (standard FFT count); binding = max
     live, iter_us, agg = live_iteration(h, p, b, torch)
     top_name, top_us = max(live, key=lambda kv: kv[1])
-    roof = roofline(p, top_us, peaks, top_name, TRAFFIC.get(top_name))
+    roof = roofline(p, top_us, peaks, top_name, TRAFFIC.get("%s@%d" % (top_name, p.n)))
     roof["share_of_iteration"] = round(top_us / iter_us, 4)
     roof["per_iteration"] = roofline(p, iter_us, peaks, "one PCG iteration (all kernels)", None)
     iteration = {"us_kernels": round(iter_us, 3), "us_per_iter_timed": round(ms * 1e3 / max(iters, 1) * world, 3),
