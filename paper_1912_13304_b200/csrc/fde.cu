@@ -26,6 +26,7 @@
 #include "sine_kernels.cuh"
 #include "dense_kernels.cuh"
 #include "tri_kernels.cuh"
+#include "sop.h"
 
 using namespace fde;
 
@@ -276,6 +277,10 @@ struct fde_handle_s {
   double2 *mu_x = nullptr, *mu_y = nullptr;
   double2 *mus_x = nullptr, *mus_y = nullptr;  // sine-domain μ_s (constant directions; sine_kernels.cuh)
   double2* mus_xn = nullptr;  // μ_s of the x direction with ν folded in (2D row pass: q̂ = ν p̂ + ... there)
+  // r02 sine-domain operator (sop.cu): DCT-split tables
+  bool sop_ok = false;
+  double *sop_hx = nullptr, *sop_hy = nullptr, *sop_mux = nullptr, *sop_muy = nullptr;
+  double2 *sop_tw = nullptr, *sop_sc = nullptr;
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
   double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
   double *invF = nullptr, *Fx = nullptr, *Fy = nullptr;
@@ -294,6 +299,7 @@ struct fde_handle_s {
   double *kx = nullptr, *kb = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kq = nullptr;
   double* kp2 = nullptr;    // second p̂ buffer of the concurrent sine body
   double* kpart = nullptr;  // fused-kernel partials [batch][3][KPMAX]
+  double* spart = nullptr;  // r02 operator pass: one p̂·q̂ partial per unit [batch][KPMAX]
   double2* zscr = nullptr;  // variable Toeplitz spectrum scratch [batch][pairs][L]
   double* V = nullptr;
   int V_cols = 0;
@@ -885,6 +891,45 @@ void build(fde_handle h, const fde_desc* d) {
     make_dir(d->alpha, h->var_x, d->dp, d->dm, 1.0, d->nu, h->mu_x, h->mus_x, h->lamS_x, h->lamK_x, h->cP_x, h->cM_x, dp, dm, &h->mus_xn);
     if (two) make_dir(d->beta, h->var_y, d->ep, d->em, ywt, 0.0, h->mu_y, h->mus_y, h->lamS_y, h->lamK_y, h->cP_y, h->cM_y, ep, em, nullptr);
   }
+  // r02 sine-domain operator (sop_kernels.cuh): 2D, constant SYMMETRIC
+  // coefficients (d+ = d-, e+ = e-: T̃ = d(T + Tᵀ) has real, even circulant
+  // eigenvalues), τ preconditioner, m = n+1 an instantiated size
+  {
+    const char* so = std::getenv("FDE_SOP");
+    const bool want = !(so && std::strcmp(so, "0") == 0);
+    h->sop_ok = want && two && !h->dense && d->prec == FDE_PREC_TAU && !h->var_x && !h->var_y && d->dp == d->dm &&
+                d->ep == d->em && fde::sop::supported(m);
+  }
+  if (h->sop_ok) {
+    // λ_k (k = 0..m) of the symmetric embedding of d(T + Tᵀ): (d+ + d-) Re λ_k
+    // of T's circulant; μ'_k = λ_k/(8m²) (sop_kernels.cuh scaling)
+    const std::vector<std::complex<double>> la = lambda(d->alpha), lb = lambda(d->beta);
+    std::vector<double> mux(m + 1), muy(m + 1), hx(n), hy(n);
+    const double s8 = 1.0 / (8.0 * (double)m * (double)m);
+    for (int k = 0; k <= m; ++k) {
+      mux[k] = (d->dp + d->dm) * la[k].real() * s8;
+      muy[k] = ywt * (d->ep + d->em) * lb[k].real() * s8;
+    }
+    for (int e = 0; e < n; ++e) {
+      hx[e] = d->nu + 0.5 * (d->dp + d->dm) * la[e + 1].real();
+      hy[e] = 0.5 * ywt * (d->ep + d->em) * lb[e + 1].real();
+    }
+    h->sop_mux = h->upload(mux);
+    h->sop_muy = h->upload(muy);
+    h->sop_hx = h->upload(hx);
+    h->sop_hy = h->upload(hy);
+    std::vector<double2> tw(m / 2), sc(m / 16);
+    for (int e = 0; e < m / 2; ++e) {
+      const auto z = root_of_unity(e, m);
+      tw[e] = make_double2(z.real(), z.imag());
+    }
+    for (int t = 0; t < m / 16; ++t) {   // (sin, cos)(πt/m) = (-Im, Re) of ω_{2m}^t, t < U = m/16
+      const auto z = root_of_unity(t, 2LL * m);
+      sc[t] = make_double2(-z.imag(), z.real());
+    }
+    h->sop_tw = h->upload(tw);
+    h->sop_sc = h->upload(sc);
+  }
 
   // preconditioner tables
   const int prec = d->prec;
@@ -1140,6 +1185,7 @@ void ensure_krylov(fde_handle h, int nvecV) {
     h->kq = h->dalloc<double>(vs);
     h->kp2 = h->dalloc<double>(vs);
     h->kpart = h->dalloc<double>((size_t)h->batch * 3 * KPMAX);
+    h->spart = h->dalloc<double>((size_t)h->batch * KPMAX);
   }
   if (nvecV > h->V_cols) {
     h->V = h->dalloc<double>(ve * nvecV);
@@ -1315,6 +1361,43 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     }
     return;
   }
+  if (h->dims == 2 && h->sop_ok) {
+    // r02 body: the even parts of both directions in one launch (sop.cu),
+    // then the vector step adding the diagonal
+    fde::sop::SopArgs sa{};
+    sa.n = h->n;
+    sa.m = h->m;
+    sa.pitch = h->sine_pitch;
+    sa.npairs = h->m / 2;
+    sa.total_warps = fde::sop::warps_for(h->m, h->batch);
+    sa.z = h->kq;   // ẑ = r̂/F (k_sine_init / k_sine_xr5)
+    sa.x = h->kx;
+    sa.p = h->kp;
+    sa.p2 = h->kp2;
+    sa.wr = h->wx;
+    sa.wc = h->wy;
+    sa.hx = h->sop_hx;
+    sa.hy = h->sop_hy;
+    sa.mux = h->sop_mux;
+    sa.muy = h->sop_muy;
+    sa.tw = h->sop_tw;
+    sa.sc = h->sop_sc;
+    sa.st = h->sst;
+    sa.ctr = h->ctr;
+    sa.part = h->spart;
+    launch_named(h, "sine_op_sop", [&] { FDE_CUDA(fde::sop::launch(sa, h->st)); });
+    KryFuse kv = kf;
+    kv.mode = KM_XR | KM_RZ | KM_GATE;
+    const double *Fx = h->Fx, *Fy = h->Fy, *wr = h->wx, *wc = h->wy, *hx = h->sop_hx, *hy = h->sop_hy;
+    const double* sp = h->spart;
+    const int n = h->n, nsp = h->m;   // one p̂·q̂ partial per unit, m units per RHS
+    int lgp = 0;
+    while ((1 << lgp) < h->sine_pitch) ++lgp;
+    launch_named(h, "sine_xr_sop", [&] {
+      launch_k(h->st, k_sine_xr5, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc, hx, hy, sp, nsp);
+    });
+    return;
+  }
   if (h->dims == 2 && h->sine_rc) {
     // concurrent body: rows + columns in one launch, then the vector step
     a.nlines = h->n;
@@ -1416,7 +1499,8 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   const int n = h->n, dims = h->dims;
   const int gx = dims == 2 ? std::min(n, KPMAX) : 64;
   const int pitch = h->sine_pitch;
-  launch_named(h, "sine_init", [&] { launch_k(h->st, k_sine_init, dim3(gx, h->batch), 256, 0, kf, n, dims, Fx, Fy, pitch); });
+  const int zout = (h->dims == 2 && h->sop_ok) ? 1 : 0;
+  launch_named(h, "sine_init", [&] { launch_k(h->st, k_sine_init, dim3(gx, h->batch), 256, 0, kf, n, dims, Fx, Fy, pitch, zout); });
   const bool persist1d = h->dims == 1 && !h->sine1d_graph;
   if (persist1d) {
     // 1D: the whole solve in ONE kernel, one CTA per RHS (the line fits in a
@@ -1448,7 +1532,7 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   } else {
     FDE_CUDA(cudaGraphLaunch(h->g_pcg, h->st));
   }
-  if (h->dims == 2 && h->sine_rc) {  // the concurrent body's last x̂ += α p̂ (lagged by one step)
+  if (h->dims == 2 && (h->sine_rc || h->sop_ok)) {  // the concurrent bodies' last x̂ += α p̂ (lagged by one step)
     KryFuse kx = kf;
     const int n = h->n;
     int lgp = 0;

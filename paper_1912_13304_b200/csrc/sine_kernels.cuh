@@ -748,6 +748,82 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr4(KryFuse k, int n, int lgp, 
   kry_reduce_finalize(k, acc);
 }
 
+// vector step of the r02 body (sop_kernels.cuh). The operator kernel wrote
+// the EVEN parts w_r, w_c of the two directions, this iteration's p̂ (row
+// units; the buffer SolveState::ppar does NOT name yet) and one p̂·q̂ partial
+// per unit (spart[rhs][0..nsp), a buffer of its own: the finalisation below
+// writes slots of KryFuse::part). Every CTA sums those partials in fixed
+// order (the same α everywhere: no grid-wide step in the operator kernel).
+// The diagonal (ν + ½λ^α_i + ½λ^β_j) p̂ is elementwise and is added here:
+// q̂ = w_r + w_c + (hx_i + hy_j) p̂, r̂ -= α q̂, ẑ = r̂/F (written for the next
+// operator pass, KryFuse::q), partials ‖r̂‖², r̂·ẑ. The finalising CTA stores
+// α (the next operator pass's lagged x̂ update) and flips ppar (KM_SOPA).
+__global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, const double* __restrict__ Fx,
+                                                     const double* __restrict__ Fy, const double* __restrict__ wr_,
+                                                     const double* __restrict__ wc_, const double* __restrict__ hx,
+                                                     const double* __restrict__ hy, const double* __restrict__ spart,
+                                                     int nsp) {
+  FDE_PDL_ENTRY();
+  const int rhs = blockIdx.y;
+  if (!k.st[rhs].cyc_active) return;
+  __shared__ double s_pq[8];
+  {
+    const double* sp = spart + (size_t)rhs * KPMAX;
+    double v = 0.0;
+    for (int i = threadIdx.x; i < nsp; i += blockDim.x) v += __ldcg(sp + i);
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) s_pq[threadIdx.x >> 5] = v;
+    __syncthreads();
+  }
+  double pq = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) pq += s_pq[w];
+  const bool spd = pq > 0.0;
+  const double al = spd ? k.st[rhs].rho / pq : 0.0;
+  const int pitch = 1 << lgp;
+  const size_t o = (size_t)rhs * ((size_t)n << lgp);
+  const int nq = (n << lgp) >> 2;
+  double* __restrict__ rr = k.r + o;
+  double* __restrict__ zz = k.q + o;
+  const double* __restrict__ wr = wr_ + o;
+  const double* __restrict__ wc = wc_ + o;
+  const double* __restrict__ pp = (k.st[rhs].ppar ? k.p : k.p2) + o;
+  const int T = gridDim.x * blockDim.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (spd) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nq; c += T) {
+      const size_t e = (size_t)c * 4;
+      dbl4 rv = ld4(rr + e);
+      const dbl4 av = ld4(wr + e), bv = ld4(wc + e), pv = ld4(pp + e);
+      const int j = (int)(e >> lgp), i = (int)e & (pitch - 1);
+      const double fy = Fy[j], dy = hy[j];
+      dbl4 zv;
+      double* rp = &rv.x;
+      double* zp = &zv.x;
+      const double* ap = &av.x;
+      const double* bp = &bv.x;
+      const double* ppv = &pv.x;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const bool ok = i + s < n;
+        const double iF = fast_rcp(ok ? Fx[i + s] + fy : 1.0);
+        const double q = ok ? fma(hx[i + s] + dy, ppv[s], ap[s] + bp[s]) : 0.0;
+        const double r = fma(-al, q, rp[s]);
+        rp[s] = r;
+        zp[s] = r * iF;
+        acc[1] = fma(r, r, acc[1]);
+        acc[2] = fma(r, zp[s], acc[2]);
+      }
+      st4(rr + e, rv);
+      st4(zz + e, zv);
+    }
+  }
+  KryFuse kk = k;
+  kk.mode = k.mode | KM_SOPA;
+  kk.xval = pq;   // every CTA summed the same partials in the same order: the finaliser's α is this CTA's α
+  kry_reduce_finalize(kk, acc);
+}
+
 // end of a concurrent-body solve: the lagged x̂ += α p̂ of the last iteration
 // (α = 0 after a breakdown exit, so nothing is pending then)
 __global__ void __launch_bounds__(256) k_sine_xfix(KryFuse k, int n, int lgp) {
@@ -770,19 +846,22 @@ __global__ void __launch_bounds__(256) k_sine_xfix(KryFuse k, int n, int lgp) {
 }
 
 // sine-domain PCG start: x̂ = 0, p̂ = 0, ‖b̂‖, ρ = Σ r̂²/F, β = 0 (r̂ = b̂ already formed)
+// zout: write ẑ_0 = r̂_0/F into KryFuse::q (the r02 body reads ẑ, k_sine_xr5
+// keeps it current) instead of zeroing it
 __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, const double* __restrict__ Fx,
-                                                   const double* __restrict__ Fy, int pitch) {
+                                                   const double* __restrict__ Fy, int pitch, int zout) {
   FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
   const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * pitch : (size_t)n);
   double acc[3] = {0.0, 0.0, 0.0};
   FDE_SINE_LOOP({
     const double rv = k.r[o + e];
+    const double iF = fast_rcp(F);
     k.x[o + e] = 0.0;
     k.p[o + e] = 0.0;
-    k.q[o + e] = 0.0;
+    k.q[o + e] = zout ? rv * iF : 0.0;
     acc[1] = fma(rv, rv, acc[1]);
-    acc[2] = fma(rv * rv, fast_rcp(F), acc[2]);
+    acc[2] = fma(rv * rv, iF, acc[2]);
   })
   if (dims == 2 && pitch > n && threadIdx.x == 0) {  // zero padding (k_sine_xr2 relies on it)
     for (int j = blockIdx.x; j < n; j += gridDim.x)

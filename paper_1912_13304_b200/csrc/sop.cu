@@ -1,0 +1,37 @@
+// Translation unit of the r02 sine-domain operator (sop_kernels.cuh) and its
+// host launcher (sop.h); compiled separately from fde.cu.
+#include <cuda_runtime.h>
+
+#include "sop.h"
+#include "sop_kernels.cuh"
+
+namespace fde {
+namespace sop {
+
+template <int U>
+static cudaError_t launch_u(const SopArgs& a, cudaStream_t st) {
+  constexpr int UPC = sop_upc<U>();
+  const size_t smem = (size_t)UPC * Geo<U>::SLOTS * sizeof(double2);
+  auto kern = k_sop<U>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<a.total_warps / UPC, U * UPC, smem, st>>>(a);   // total_warps: units over the batch
+  return cudaGetLastError();
+}
+
+bool supported(int m) { return m == 512 || m == 1024 || m == 2048 || m == 4096; }
+
+cudaError_t launch(const SopArgs& a, cudaStream_t st) {
+  switch (a.m) {
+    case 512: return launch_u<32>(a, st);
+    case 1024: return launch_u<64>(a, st);
+    case 2048: return launch_u<128>(a, st);
+    case 4096: return launch_u<256>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int warps_for(int m, int batch) { return batch * m; }   // units (CTAs): 2·npairs = m per RHS
+
+}  // namespace sop
+}  // namespace fde
