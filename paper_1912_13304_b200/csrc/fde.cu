@@ -1602,15 +1602,18 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
   // partials instead of 592)
   auto ggrid = [&](int chunk) { return dim3(std::min(RED_BLOCKS, std::max(1, (va.N + chunk - 1) / chunk)), h->batch); };
   if (h->gm_dcgs && restart <= 31) {  // DCGS2: two passes over the basis per step (krylov_kernels.cuh)
+    // pass A: warp-split (k_gm_dcgs_a, measured best: the barrier-free a2/a3
+    // variants were slower); pass B: streaming, one thread per element (b2)
+    const dim3 sgrid(std::min(RED_BLOCKS, std::max(1, (va.N + 127) / 128)), h->batch);
     auto pick = [&](int j, auto&& f) {
-      if (j < 8) f(std::integral_constant<int, 1>{}, std::integral_constant<int, 16>{});
-      else if (j < 16) f(std::integral_constant<int, 2>{}, std::integral_constant<int, 8>{});
-      else f(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{});
+      if (j < 8) f(std::integral_constant<int, 1>{}, std::integral_constant<int, 16>{}, std::integral_constant<int, 8>{});
+      else if (j < 16) f(std::integral_constant<int, 2>{}, std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{});
+      else f(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}, std::integral_constant<int, 32>{});
     };
     for (int j = 0; j <= restart; ++j) {
       double* Vj = V + (size_t)j * vs;
       if (j == restart) {  // end of cycle: reorthogonalise u_m, finalise column m-1
-        pick(j, [&](auto NS, auto EPL) {
+        pick(j, [&](auto NS, auto EPL, auto) {
           launch_named(h, "gm_dcgs_a", [&] {
             launch_k(h->st, k_gm_dcgs_a<decltype(NS)::value, decltype(EPL)::value>, ggrid(32 * decltype(EPL)::value),
                      RED_THREADS, 0, va, V, vs, (const double*)Vj, (const double*)nullptr, j);
@@ -1626,15 +1629,13 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
         op_matvec(h, Vj, h->kq, gA);
         op_tau(h, h->kq, Vn, gA);
       }
-      pick(j, [&](auto NS, auto EPL) {
-        constexpr int ns = decltype(NS)::value, epl = decltype(EPL)::value;
+      pick(j, [&](auto NS, auto EPL, auto JB) {
+        constexpr int ns = decltype(NS)::value, epl = decltype(EPL)::value, jb = decltype(JB)::value;
         launch_named(h, "gm_dcgs_a", [&] {
           launch_k(h->st, k_gm_dcgs_a<ns, epl>, ggrid(32 * epl), RED_THREADS, 0, va, V, vs, (const double*)Vj,
                    (const double*)Vn, j);
         });
-        launch_named(h, "gm_dcgs_b", [&] {
-          launch_k(h->st, k_gm_dcgs_b<ns, epl>, ggrid(32 * (epl > 8 ? 8 : epl)), RED_THREADS, 0, va, V, vs, Vj, Vn, j);
-        });
+        launch_named(h, "gm_dcgs_b", [&] { launch_k(h->st, k_gm_dcgs_b2<jb>, sgrid, 128, 0, va, V, vs, Vj, Vn, j); });
       });
     }
   } else

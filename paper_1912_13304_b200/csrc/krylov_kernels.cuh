@@ -567,8 +567,9 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
       ssn[i] = __ldcg(&gs.sn[i]);
     }
   }
-  if (threadIdx.x == 32) s_nu = __ldcg(&gs.h[2 * j]);
-  if (threadIdx.x == 64 && j >= 1) s_g = __ldcg(&gs.g[j - 1]);
+  // (any block size: the passes run with 32..256 threads)
+  if (threadIdx.x == (32 % blockDim.x)) s_nu = __ldcg(&gs.h[2 * j]);
+  if (threadIdx.x == (64 % blockDim.x) && j >= 1) s_g = __ldcg(&gs.g[j - 1]);
   __syncthreads();
   if (threadIdx.x == 0) {
     const double nu = s_nu;
@@ -729,77 +730,43 @@ __global__ void __launch_bounds__(256) k_gm_dcgs_a(VecArgs a, const double* __re
   }
 }
 
-// pass B: q_j (into u's slot) and u_{j+1} (into z's slot)
-template <int NS, int EPL0>
-__global__ void __launch_bounds__(256) k_gm_dcgs_b(VecArgs a, const double* __restrict__ V, size_t vstride,
-                                                   double* __restrict__ u, double* __restrict__ z, int j) {
+// Pass B, streaming (r02): one thread per element (grid-stride), every basis
+// vector of the element loaded together, q_j and u_{j+1} formed in
+// registers; no shared-memory staging and no barrier in the element loop
+// (JB = the compile-time bound of j: 8, 16 or 32). Measured faster than the
+// warp-split pass B it replaced (cfg 4: 40 vs 42 µs per step); the same idea
+// for pass A (register accumulators, or warp-split without staging) measured
+// slower than k_gm_dcgs_a and was dropped.
+template <int JB>
+__global__ void __launch_bounds__(128) k_gm_dcgs_b2(VecArgs a, const double* __restrict__ V, size_t vstride,
+                                                    double* __restrict__ u, double* __restrict__ z, int j) {
   FDE_PDL_ENTRY();
-  constexpr int EPL = EPL0 > 8 ? 8 : EPL0;  // two 8 x CH partial arrays in 48 KB of static shared memory
-  constexpr int CH = 32 * EPL;
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
   const size_t o = (size_t)rb * N;
-  const int nv = j;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __shared__ double pa[8][CH], pb[8][CH];
-  __shared__ double ca[32], cb[32];
+  __shared__ double ca[JB], cb[JB];
   const GmresSmall& gs = a.gs[rb];
-  for (int i = threadIdx.x; i < 32; i += blockDim.x) {
-    ca[i] = i < nv ? __ldcg(&gs.h2[i]) : 0.0;
-    cb[i] = i < nv ? __ldcg(&gs.h2[32 + i]) : 0.0;
+  for (int i = threadIdx.x; i < JB; i += blockDim.x) {
+    ca[i] = i < j ? __ldcg(&gs.h2[i]) : 0.0;
+    cb[i] = i < j ? __ldcg(&gs.h2[32 + i]) : 0.0;
   }
   const double dj = __ldcg(&gs.dj), bi = __ldcg(&gs.binv);
   __syncthreads();
-  constexpr int TPT = (CH + 255) / 256;
-  for (long long c0 = (long long)blockIdx.x * CH; c0 < N; c0 += (long long)gridDim.x * CH) {
-    double vv[NS][EPL];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N; e += gridDim.x * blockDim.x) {
+    const double uv = __ldcg(u + o + e), zv = __ldcg(z + o + e);
+    double vv[JB];
 #pragma unroll
-    for (int sl = 0; sl < NS; ++sl) {
-      const int i = wid + 8 * sl;
+    for (int i = 0; i < JB; ++i) vv[i] = i < j ? __ldcg(V + (size_t)i * vstride + o + e) : 0.0;
+    double sa = 0.0, sb = 0.0;
 #pragma unroll
-      for (int q = 0; q < EPL; ++q) {
-        const long long e = c0 + lane + 32 * q;
-        vv[sl][q] = (i < nv && e < N) ? __ldg(V + (size_t)i * vstride + o + e) : 0.0;
-      }
+    for (int i = 0; i < JB; ++i) {
+      sa = fma(ca[i], vv[i], sa);
+      sb = fma(cb[i], vv[i], sb);
     }
-    double uv[TPT], zv[TPT];
-#pragma unroll
-    for (int q = 0; q < TPT; ++q) {
-      const int t = threadIdx.x + 256 * q;
-      const long long e = c0 + t;
-      uv[q] = (t < CH && e < N) ? u[o + e] : 0.0;
-      zv[q] = (t < CH && e < N) ? z[o + e] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < EPL; ++q) {
-      double sa = 0.0, sb = 0.0;
-#pragma unroll
-      for (int sl = 0; sl < NS; ++sl) {
-        sa = fma(ca[wid + 8 * sl], vv[sl][q], sa);
-        sb = fma(cb[wid + 8 * sl], vv[sl][q], sb);
-      }
-      pa[wid][lane + 32 * q] = sa;
-      pb[wid][lane + 32 * q] = sb;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < TPT; ++q) {
-      const int t = threadIdx.x + 256 * q;
-      const long long e = c0 + t;
-      if (t < CH && e < N) {
-        double SA = 0.0, SB = 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          SA += pa[k][t];
-          SB += pb[k][t];
-        }
-        const double qv = (uv[q] - SA) * bi;
-        u[o + e] = qv;
-        z[o + e] = (zv[q] - SB - dj * qv) * bi;
-      }
-    }
-    __syncthreads();
+    const double qv = (uv - sa) * bi;
+    u[o + e] = qv;
+    z[o + e] = (zv - sb - dj * qv) * bi;
   }
 }
 
