@@ -50,12 +50,11 @@ struct FdeFail {
                     std::string(#call) + ": " + cudaGetErrorString(e_)};                \
   } while (0)
 
-// Every kernel launch goes through cudaLaunchKernelEx; with FDE_PDL=1 it
-// carries programmatic stream serialisation (PDL, see FDE_PDL_ENTRY). Off by
-// default: measured on the B200 it did not help (cfg 5 n=1023 11.2k vs 11.5k
-// PCG it/s, cfg 3 69.6 vs 51.5 µs/iteration) — the early-launched dependent
-// CTAs hold SM slots while they wait.
-bool g_pdl = false;
+// Every kernel launch goes through cudaLaunchKernelEx. Programmatic dependent
+// launch (PDL) measured slower on the B200 in r01 (cfg 5 n=1023 11.2k vs
+// 11.5k PCG it/s, cfg 3 69.6 vs 51.5 µs/iteration: the early-launched
+// dependent CTAs hold SM slots while they wait), so it is not requested.
+constexpr bool g_pdl = false;
 template <typename... KArgs, typename... Args>
 void launch_k(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -316,15 +315,8 @@ struct fde_handle_s {
 
   bool force_standard_pcg = false;  // env FDE_PCG=standard (A/B against the sine-domain PCG)
   bool gm_dcgs = true;              // GMRES orthogonalisation by DCGS2 (FDE_GM_ORTH=cgs2: classical CGS2)
-  bool gm_ws = true;                // warp-split CGS kernels for j < 32 (FDE_GM_WS=0: one thread per element)
-  bool sine_xr4 = true;             // 32-byte vector step of the concurrent body (FDE_XR4=0: 16-byte)
-  bool sine_xr_rows = false;        // FDE_SINE_XR=rows: the per-row vector step instead of the flat one
-  bool sine_rc = true;              // 2D sine body as one concurrent row+column launch (else two passes)
-  bool sine_pqs = true;             // p̂·q̂ of the 2D sine body from the spectra (FDE_SINE_PQ=direct: elementwise)
   bool no_graph = false;            // env FDE_GRAPH=0: host-driven loop (for profilers)
   int sine_pitch = 0;               // row pitch of the sine-domain PCG's internal 2D vectors (n+1)
-  bool sine_legacy = true;          // 3-kernel sine-domain body; env FDE_SINE_BODY=2: the recurrence body (A/B)
-  bool sine1d_graph = false;        // env FDE_SINE1D=graph: 1D PCG per-iteration graph instead of one persistent kernel
   std::vector<void*> allocs;
   // profiling (fde_profile_unit)
   bool prof = false;
@@ -1027,30 +1019,16 @@ void build(fde_handle h, const fde_desc* d) {
   h->gsm = h->dalloc<GmresSmall>(h->batch);
   h->ctr = h->dalloc<Counters>(1);
   {
+    // runtime switches (each one A/B-tested by the GPU suite): FDE_PCG=standard
+    // (standard-basis fused PCG instead of the sine domain), FDE_SOP=0 (r01
+    // concurrent body instead of r02), FDE_GM_ORTH=cgs2 (CGS2 instead of
+    // DCGS2), FDE_GRAPH=0 (host-driven loop for profilers)
     const char* e = std::getenv("FDE_PCG");
     h->force_standard_pcg = e && std::strcmp(e, "standard") == 0;
     const char* g = std::getenv("FDE_GRAPH");
     h->no_graph = g && std::strcmp(g, "0") == 0;
-    const char* sb = std::getenv("FDE_SINE_BODY");
-    h->sine_legacy = !(sb && std::strcmp(sb, "2") == 0);
-    const char* pq = std::getenv("FDE_SINE_PQ");
-    h->sine_pqs = !(pq && std::strcmp(pq, "direct") == 0);
-    // concurrent body where it measured faster on the B200 (n <= 2047, any
-    // batch); FDE_SINE_RC=1 / 0 forces it on / off
-    const char* rc = std::getenv("FDE_SINE_RC");
-    h->sine_rc = rc ? std::strcmp(rc, "0") != 0 : (n <= 2047);
     const char* go = std::getenv("FDE_GM_ORTH");
     h->gm_dcgs = !(go && std::strcmp(go, "cgs2") == 0);
-    const char* gw = std::getenv("FDE_GM_WS");
-    h->gm_ws = !(gw && std::strcmp(gw, "0") == 0);
-    const char* x4 = std::getenv("FDE_XR4");
-    h->sine_xr4 = !(x4 && std::strcmp(x4, "0") == 0);
-    const char* xe = std::getenv("FDE_SINE_XR");
-    h->sine_xr_rows = xe && std::strcmp(xe, "rows") == 0;
-    const char* s1 = std::getenv("FDE_SINE1D");
-    h->sine1d_graph = s1 && std::strcmp(s1, "graph") == 0;
-    const char* pd = std::getenv("FDE_PDL");
-    g_pdl = pd && std::strcmp(pd, "1") == 0;
   }
   h->part = h->dalloc<double>((size_t)h->batch * (MAX_RESTART + 1) * RED_BLOCKS);
   FDE_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->st));
@@ -1317,53 +1295,31 @@ void op_dst_all(fde_handle h, const double* x, double* y, double oscale) {
   FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, true, false>(h, b)));
 }
 
-int xr_grid() {  // CTAs of the sine-domain vector step (FDE_XR_GRID)
-  static const int g = [] {
-    const char* e = std::getenv("FDE_XR_GRID");
-    return e ? std::atoi(e) : 592;
-  }();
-  return g;
-}
-
+// One PCG iteration in the sine domain (the loop body of the solve graph):
+// 1D = one recurrence body (MODE 5, the kernel the persistent 1D solve
+// repeats); 2D = the r02 body (sop.cu: even parts of both directions, then
+// the vector step adding the diagonal) for n+1 in {512..4096}, else the r01
+// concurrent body (k_sineop_rc + k_sine_xr4).
+constexpr int XR_GRID = 592;   // CTAs of the sine-domain vector steps (4 per SM)
 void sine_iteration(fde_handle h, double rtol, int maxit) {
   KryFuse kf = make_kf(h, rtol, maxit);
   LineArgs a = base_args(h);
   a.Fx = h->Fx;
   a.Fy = h->dims == 2 ? h->Fy : nullptr;
   a.mu = h->mus_x;
-  if (!h->sine_legacy) {
-    // body k: 2D = rows (r, x update, ẑ = r/F, convergence, β) + columns (q = Aẑ + βq,
-    // p = ẑ + βp, α); 1D = one kernel with CTA-local reductions
-    if (h->dims == 2) {
-      a.nlines = h->n;
-      a.y = h->wx;
-      a.kf = kf;
-      a.kf.mode = KM_SROW | KM_GATE;
-      FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 3>(h, a)));
-      LineArgs b = base_args(h);
-      b.Fx = h->Fx;
-      b.Fy = h->Fy;
-      b.nlines = h->n;
-      b.yin = h->wx;
-      b.y = h->kq;
-      b.mu = h->mus_y;
-      b.nu = h->d.nu;
-      b.kf = kf;
-      b.kf.mode = KM_PQ | KM_GATE;
-      FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, true, 4>(h, b)));
-    } else {
-      a.nlines = 1;
-      a.y = h->kq;
-      a.nu = h->d.nu;
-      a.kf = kf;
-      a.kf.mode = KM_GATE;
-      FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 5>(h, a)));
-    }
+  if (h->dims == 1) {
+    a.nlines = 1;
+    a.y = h->kq;
+    a.nu = h->d.nu;
+    a.kf = kf;
+    a.kf.mode = KM_GATE;
+    FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 5>(h, a)));
     return;
   }
-  if (h->dims == 2 && h->sop_ok) {
-    // r02 body: the even parts of both directions in one launch (sop.cu),
-    // then the vector step adding the diagonal
+  int lgp = 0;
+  while ((1 << lgp) < h->sine_pitch) ++lgp;
+  if ((1 << lgp) != h->sine_pitch || lgp < 2) throw FdeFail{FDE_ERR_UNSUPPORTED, "sine pitch is not a power of two"};
+  if (h->sop_ok) {
     fde::sop::SopArgs sa{};
     sa.n = h->n;
     sa.m = h->m;
@@ -1391,91 +1347,27 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     const double *Fx = h->Fx, *Fy = h->Fy, *wr = h->wx, *wc = h->wy, *hx = h->sop_hx, *hy = h->sop_hy;
     const double* sp = h->spart;
     const int n = h->n, nsp = h->m;   // one p̂·q̂ partial per unit, m units per RHS
-    int lgp = 0;
-    while ((1 << lgp) < h->sine_pitch) ++lgp;
     launch_named(h, "sine_xr_sop", [&] {
-      launch_k(h->st, k_sine_xr5, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc, hx, hy, sp, nsp);
+      launch_k(h->st, k_sine_xr5, dim3(XR_GRID, h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc, hx, hy, sp, nsp);
     });
     return;
   }
-  if (h->dims == 2 && h->sine_rc) {
-    // concurrent body: rows + columns in one launch, then the vector step
-    a.nlines = h->n;
-    a.x = h->kr;
-    a.y = h->wx;
-    a.mu = h->mus_xn;
-    a.kf = kf;
-    a.kf.mode = KM_PQ | KM_PQS | KM_GATE | KM_PFLIP;
-    LineArgs c = a;
-    c.y = h->wy;
-    c.mu = h->mus_y;
-    FDE_SWITCH_K(h->K, (launch_sineop_rc_k<KK - 1>(h, a, c)));
-    KryFuse kv = kf;
-    kv.mode = KM_XR | KM_RZ | KM_GATE;
-    const double* Fx = h->Fx;
-    const double* Fy = h->Fy;
-    const double *wr = h->wx, *wc = h->wy;
-    const int n = h->n, pitch = h->sine_pitch;
-    int lgp = 0;
-    while ((1 << lgp) < pitch) ++lgp;
-    if ((1 << lgp) != pitch) throw FdeFail{FDE_ERR_UNSUPPORTED, "sine pitch is not a power of two"};
-    if (h->sine_xr4 && lgp >= 2)
-      launch_named(h, "sine_xr_rc", [&] { launch_k(h->st, k_sine_xr4, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc); });
-    else
-      launch_named(h, "sine_xr_rc", [&] { launch_k(h->st, k_sine_xr3, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc); });
-    return;
-  }
-  if (h->dims == 2) {
-    a.nlines = h->n;
-    a.x = h->kr;
-    a.y = h->wx;
-    a.kf = kf;
-    a.kf.mode = KM_PUPD | KM_GATE;
-    if (h->sine_pqs) {  // p̂·q̂ from the spectra of both passes, ν folded into the row multiplier
-      a.mu = h->mus_xn;
-      a.kf.mode |= KM_PQS | KM_PQX;
-    }
-    int rows_grid = 0;
-    FDE_SWITCH_K(h->K, (rows_grid = launch_sineop_k<KK - 1, false, 0>(h, a)));
-    if (rows_grid > KPMAX / 2) throw FdeFail{FDE_ERR_UNSUPPORTED, "row pass grid exceeds the partial region"};
-    LineArgs b = base_args(h);
-    b.nlines = h->n;
-    b.x = h->kp;
-    b.yin = h->wx;
-    b.y = h->kq;
-    b.mu = h->mus_y;
-    b.nu = h->d.nu;
-    b.kf = kf;
-    b.kf.mode = KM_PQ | KM_GATE;
-    if (h->sine_pqs) {
-      b.nu = 0.0;
-      b.kf.mode |= KM_PQS;
-      b.kf.xpart = rows_grid;
-    }
-    FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, true, 1>(h, b)));
-  } else {
-    a.nlines = 1;
-    a.x = h->kr;
-    a.y = h->kq;
-    a.nu = h->d.nu;
-    a.kf = kf;
-    a.kf.mode = KM_PUPD | KM_PQ | KM_GATE;
-    FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 2>(h, a)));
-  }
+  // r01 concurrent body: rows + columns in one launch, then the vector step
+  a.nlines = h->n;
+  a.x = h->kr;
+  a.y = h->wx;
+  a.mu = h->mus_xn;
+  a.kf = kf;
+  a.kf.mode = KM_PQ | KM_PQS | KM_GATE | KM_PFLIP;
+  LineArgs c = a;
+  c.y = h->wy;
+  c.mu = h->mus_y;
+  FDE_SWITCH_K(h->K, (launch_sineop_rc_k<KK - 1>(h, a, c)));
   KryFuse kv = kf;
   kv.mode = KM_XR | KM_RZ | KM_GATE;
-  const double* Fx = h->Fx;
-  const double* Fy = h->dims == 2 ? h->Fy : nullptr;
-  const int n = h->n, dims = h->dims;
-  const int gx = dims == 2 ? std::min(n, xr_grid()) : 64;
-  const int pitch = h->sine_pitch;
-  if (dims == 2 && (pitch & (pitch - 1)) == 0 && !h->sine_xr_rows) {
-    int lgp = 0;
-    while ((1 << lgp) < pitch) ++lgp;
-    launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr2, dim3(xr_grid(), h->batch), 256, 0, kv, n, lgp, Fx, Fy); });
-  } else {
-    launch_named(h, "sine_xr", [&] { launch_k(h->st, k_sine_xr, dim3(gx, h->batch), 256, 0, kv, n, dims, Fx, Fy, pitch); });
-  }
+  const double *Fx = h->Fx, *Fy = h->Fy, *wr = h->wx, *wc = h->wy;
+  const int n = h->n;
+  launch_named(h, "sine_xr_rc", [&] { launch_k(h->st, k_sine_xr4, dim3(XR_GRID, h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc); });
 }
 
 fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, int maxit, fde_stats* st) {
@@ -1501,7 +1393,7 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   const int pitch = h->sine_pitch;
   const int zout = (h->dims == 2 && h->sop_ok) ? 1 : 0;
   launch_named(h, "sine_init", [&] { launch_k(h->st, k_sine_init, dim3(gx, h->batch), 256, 0, kf, n, dims, Fx, Fy, pitch, zout); });
-  const bool persist1d = h->dims == 1 && !h->sine1d_graph;
+  const bool persist1d = h->dims == 1 && !h->no_graph;
   if (persist1d) {
     // 1D: the whole solve in ONE kernel, one CTA per RHS (the line fits in a
     // CTA, so both reductions of a body are CTA-local; recurrence body MODE 5)
@@ -1532,12 +1424,12 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
   } else {
     FDE_CUDA(cudaGraphLaunch(h->g_pcg, h->st));
   }
-  if (h->dims == 2 && (h->sine_rc || h->sop_ok)) {  // the concurrent bodies' last x̂ += α p̂ (lagged by one step)
+  if (h->dims == 2) {  // the 2D bodies' last x̂ += α p̂ (lagged by one step)
     KryFuse kx = kf;
     const int n = h->n;
     int lgp = 0;
     while ((1 << lgp) < h->sine_pitch) ++lgp;
-    launch_named(h, "sine_xfix", [&] { launch_k(h->st, k_sine_xfix, dim3(xr_grid(), h->batch), 256, 0, kx, n, lgp); });
+    launch_named(h, "sine_xfix", [&] { launch_k(h->st, k_sine_xfix, dim3(XR_GRID, h->batch), 256, 0, kx, n, lgp); });
   }
   // x = (S⊗S) x̂ = (D⊗D) x̃ / (2m)^dims
   const double s = 1.0 / (2.0 * h->m);
@@ -1649,7 +1541,7 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
       op_matvec(h, Vj, h->kq, gA);
       op_tau(h, h->kq, Vn, gA);
     }
-    if (j < 32 && h->gm_ws) {  // warp-split CGS passes (krylov_kernels.cuh)
+    if (j < 32) {  // warp-split CGS passes (krylov_kernels.cuh); beyond: one thread per element
       auto cgs = [&](int chunk, auto k0, auto k1, auto k2) {
         const dim3 gg = ggrid(chunk);
         launch_named(h, "gm_mdot", [&] { launch_k(h->st, k0, gg, RED_THREADS, 0, va, V, vs, Vn, j); });

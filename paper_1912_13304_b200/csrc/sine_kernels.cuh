@@ -69,31 +69,25 @@ __device__ __forceinline__ double symbol_at(const LineArgs& a, int l, int e) {
   return COL ? a.Fx[l] + a.Fy[e] : a.Fx[e] + a.Fy[l];
 }
 
-// Two loop bodies are implemented. The recurrence body (MODES 3-5,
-// FDE_SINE_BODY=2) uses the standard recurrence q = A z + β q (p = z + β p):
-// MODE 3: 2D rows, body k: r̂ -= α q̂, x̂ += α p̂ (α_{k-1}; written back),
-//         ẑ = r̂/F, partials ‖r̂‖², r̂·ẑ (KM_SROW: convergence, β_k), y = (S T̃_α S) ẑ
-// MODE 4: 2D columns: w = ν ẑ + yin + (S T̃_β S) ẑ, q̂ = w + β q̂, p̂ = ẑ + β p̂
-//         (written back), partial p̂·q̂ (KM_PQ: α_k)
-// MODE 5: 1D, one CTA per RHS: MODE 3 + MODE 4 in one kernel, both
-//         reductions inside the CTA (no grid-wide step at all)
-// so a 2D iteration is 2 kernels and a 1D one is 1 — but measured slower on
-// the B200 (cfg 5 n=1023: 148 vs 90 µs/iteration): the column pass then does
-// the vector recurrences in the strided column layout. The default body
-// (MODES 0-2 + k_sine_xr, 3 kernels) applies the operator to p̂:
-// MODE 0: 2D row pass:   p̂ = r̂/F + β p̂ (written back), y = (S T̃_α S) p̂ along rows
-// MODE 1: 2D column pass: y = q̂ = ν p̂ + yin + (S T̃_β S) p̂ along columns, partial p̂·q̂
-// MODE 2: 1D:            p̂ = r̂/F + β p̂, y = q̂ = ν p̂ + (S T̃ S) p̂, partial p̂·q̂
-// a.x = r̂ (MODE 0/2) or p̂ (MODE 1); a.kf.p = p̂; a.mu = the sine-domain μ_s.
-// MODE 6/7: the concurrent body (k_sineop_rc): row (6) and column (7) passes
-// of ONE launch, independent of each other: both form p̂ = r̂/F + β p̂_old on
-// the fly (not written back), apply their direction's operator and write it
-// (6: w_r = ν p̂ + (S T̃_α S) p̂ rows, ν in μ; 7: w_c = (S T̃_β S) p̂ columns);
-// p̂·q̂ = p̂·w_r + p̂·w_c from the spectra (KM_PQS), α by the launch's last CTA.
-// the row units also write p̂ (into the other p̂ buffer: SolveState::ppar) and
-// apply the lagged x̂ update; k_sine_xr3/4 form q̂ = w_r + w_c for the vector step.
+// Loop bodies (r01 DST -> length-2m Toeplitz -> DST route; the 2D sizes
+// n+1 in {512..4096} run the r02 body of sop_kernels.cuh instead):
+// MODE 5: 1D, one CTA per RHS, the recurrence body q = A z + β q (p = z + β p):
+//         r̂ -= α q̂, x̂ += α p̂ (α_{k-1}, written back), ẑ = r̂/F, ‖r̂‖²
+//         (iterations, convergence) and r̂·ẑ (β) inside the CTA, then
+//         q̂ = ν ẑ + (S T̃ S) ẑ + β q̂, p̂ = ẑ + β p̂ and p̂·q̂ (α) inside the CTA;
+//         with a.persist the CTA repeats the body until its RHS finishes (the
+//         whole 1D solve is one kernel).
+// MODE 6/7: the concurrent 2D body (k_sineop_rc): row (6) and column (7)
+//         passes of ONE launch, independent of each other: both form
+//         p̂ = r̂/F + β p̂_old on the fly, apply their direction's operator and
+//         write it (6: w_r = ν p̂ + (S T̃_α S) p̂ along rows, ν in μ; 7: w_c =
+//         (S T̃_β S) p̂ along columns); p̂·q̂ = p̂·w_r + p̂·w_c from the spectra,
+//         α by the launch's last CTA; the row units also write p̂ (into the
+//         other p̂ buffer: SolveState::ppar) and apply the lagged x̂ update;
+//         k_sine_xr4 forms q̂ = w_r + w_c for the vector step.
 template <int KM, bool COL, int FPC, int MODE>
 __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
+  static_assert(MODE == 5 || MODE == 6 || MODE == 7, "sine body modes: 5 (1D), 6/7 (2D concurrent)");
   using GD = FftGeom<KM, sine_kd(KM)>;           // DST: length-m FFT, 2^KD points per thread
   using GT = FftGeom<KM + 1, sine_kd(KM) + 1>;   // Toeplitz: length-2m FFT, 2^(KD+1) points per thread
   static_assert(GD::P == GT::P, "one thread layout for both transforms");
@@ -104,8 +98,7 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
   FDE_PROBE(0);
   const int f = M::group(), t = M::lane();
   double2* sm = smem_all + (size_t)f * GT::SM_STRIDE;
-  double2* smW = smem_all + (size_t)FPC * GT::SM_STRIDE + (size_t)f * GD::SM_STRIDE;
-  double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * (GT::SM_STRIDE + ((MODE == 1 || MODE == 4) ? GD::SM_STRIDE : 0)));
+  double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * GT::SM_STRIDE);
   const TwSrc twd{nullptr, a.twpm}, twt{nullptr, a.twp};
   const int g = bx * FPC + f;
   const int l0 = 2 * g, l1 = 2 * g + 1;
@@ -122,20 +115,20 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
   for (;;) {  // one loop body; MODE 5 with a.persist repeats it until the RHS finishes
   // 1. stage the operator input in shared memory (natural order)
   SolveState* const sst = a.kf.st + blockIdx.y;
-  const double beta = (MODE == 0 || MODE == 2 || MODE == 6 || MODE == 7) ? sst->betac : 0.0;
+  const double beta = (MODE >= 6) ? sst->betac : 0.0;
   // MODE 6/7 read p̂_old from the buffer SolveState::ppar names; MODE 6 writes
   // p̂_new into the other one (the column units read p̂_old concurrently)
   const int ppar = (MODE >= 6) ? sst->ppar : 0;
   const double* const pold = (MODE >= 6 && ppar) ? a.kf.p2 : a.kf.p;
   double* const pnew = (MODE >= 6 && ppar) ? a.kf.p : a.kf.p2;
-  // MODE 6 applies the lagged x̂ += α_{k-1} p̂_{k-1} (k_sine_xr3/4 leave x̂ alone)
-  const double alpha = (MODE == 3 || MODE == 5 || MODE == 6) ? sst->alpha : 0.0;
+  // MODE 5 and 6 apply the lagged x̂ += α_{k-1} p̂_{k-1}
+  const double alpha = (MODE == 5 || MODE == 6) ? sst->alpha : 0.0;
   double acc[3] = {0.0, 0.0, 0.0};
   {
     // phase 1: every global load of this thread's RD elements (no stores in
     // between, so they are all in flight together); phase 2: arithmetic,
     // write-backs and the shared-memory staging
-    constexpr int NV = (MODE == 3 || MODE == 5) ? 4 : (MODE == 6 ? 3 : ((MODE == 0 || MODE == 2 || MODE == 7) ? 2 : 1));
+    constexpr int NV = MODE == 5 ? 4 : (MODE == 6 ? 3 : 2);
     double g0v[NV][RD], g1v[NV][RD], f0v[RD], f1v[RD];
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
@@ -143,12 +136,9 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
       const bool ok = e < n;
       const long long o0 = A0.base + (long long)(ok ? e : 0) * A0.stride, o1 = A1.base + (long long)(ok ? e : 0) * A1.stride;
       const double* src[4];
-      if (MODE == 3 || MODE == 5) { src[0] = a.kf.r; src[1] = a.kf.q; src[2] = a.kf.p; src[3] = a.kf.x; }
+      if (MODE == 5) { src[0] = a.kf.r; src[1] = a.kf.q; src[2] = a.kf.p; src[3] = a.kf.x; }
       else if (MODE == 6) { src[0] = a.x; src[1] = pold; src[2] = a.kf.x; }
-      else if (MODE == 7) { src[0] = a.x; src[1] = pold; }
-      else if (MODE == 0 || MODE == 2) { src[0] = a.x; src[1] = a.kf.p; }
-      else if (MODE == 4) { src[0] = a.kf.r; }
-      else { src[0] = a.x; }
+      else { src[0] = a.x; src[1] = pold; }
 #pragma unroll
       for (int c = 0; c < NV; ++c) {
         if (vec2) {
@@ -160,10 +150,8 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
           g1v[c][i] = (ok && v1) ? src[c][o1] : 0.0;
         }
       }
-      if (MODE != 1) {
-        f0v[i] = (ok && v0) ? symbol_at<COL>(a, l0, e) : 1.0;
-        f1v[i] = (ok && v1) ? symbol_at<COL>(a, l1, e) : 1.0;
-      }
+      f0v[i] = (ok && v0) ? symbol_at<COL>(a, l0, e) : 1.0;
+      f1v[i] = (ok && v1) ? symbol_at<COL>(a, l1, e) : 1.0;
     }
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
@@ -171,12 +159,7 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
       if (e >= n) continue;
       const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
       double p0 = 0.0, p1 = 0.0;
-      if (MODE == 0 || MODE == 2) {  // p̂ = ẑ + β p̂ with ẑ = r̂ / F (the τ-solve is diagonal here)
-        p0 = fma(beta, g0v[1][i], g0v[0][i] * fast_rcp(f0v[i]));
-        p1 = fma(beta, g1v[1][i], g1v[0][i] * fast_rcp(f1v[i]));
-        if (v0) a.kf.p[o0] = p0;
-        if (v1) a.kf.p[o1] = p1;
-      } else if (MODE >= 6) {  // p̂ = ẑ + β p̂_old
+      if (MODE >= 6) {  // p̂ = ẑ + β p̂_old
         p0 = fma(beta, g0v[1][i], g0v[0][i] * fast_rcp(f0v[i]));
         p1 = fma(beta, g1v[1][i], g1v[0][i] * fast_rcp(f1v[i]));
         if (MODE == 6) {  // p̂_new and the lagged x̂ update of the previous iteration (rows: coalesced)
@@ -189,7 +172,7 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
             a.kf.x[o1] = fma(alpha, g1v[1][i], g1v[NV - 1][i]);
           }
         }
-      } else if (MODE == 3 || MODE == 5) {  // r̂ -= α q̂, x̂ += α p̂, ẑ = r̂/F
+      } else {  // MODE 5: r̂ -= α q̂, x̂ += α p̂, ẑ = r̂/F
         const double r0 = fma(-alpha, g0v[1][i], g0v[0][i]), r1 = fma(-alpha, g1v[1][i], g1v[0][i]);
         p0 = r0 * fast_rcp(f0v[i]);
         p1 = r1 * fast_rcp(f1v[i]);
@@ -203,12 +186,6 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
         }
         acc[1] = fma(r0, r0, fma(r1, r1, acc[1]));
         acc[2] = fma(r0, p0, fma(r1, p1, acc[2]));
-      } else if (MODE == 4) {  // ẑ = r̂/F
-        p0 = g0v[0][i] * fast_rcp(f0v[i]);
-        p1 = g1v[0][i] * fast_rcp(f1v[i]);
-      } else {
-        p0 = g0v[0][i];
-        p1 = g1v[0][i];
       }
       sm[GD::swz(e)] = make_double2(p0, p1);
     }
@@ -241,23 +218,6 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
     beta5 = scr[0];
     __syncthreads();
   }
-#ifndef FDE_SINE_YIN_ASYNC
-#define FDE_SINE_YIN_ASYNC 1
-#endif
-  if (FDE_SINE_YIN_ASYNC && (MODE == 1 || MODE == 4) && a.yin) {  // the row pass's result streams in for the epilogue (chunk layout)
-#pragma unroll
-    for (int i = 0; i < RD; ++i) {
-      const int e = RD * t + i - 1;
-      if (e >= 0 && e < n) {
-        if (vec2) {
-          cp_async16(&smW[GD::swz(e)], a.yin + A0.base + (long long)e * A0.stride);
-        } else {
-          if (v0) cp_async8(&smW[GD::swz(e)].x, a.yin + A0.base + (long long)e * A0.stride);
-          if (v1) cp_async8(&smW[GD::swz(e)].y, a.yin + A1.base + (long long)e * A1.stride);
-        }
-      }
-    }
-  }
   __syncthreads();
 
   FDE_PROBE(1);
@@ -287,7 +247,7 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
   for (int q = GT::R / 2; q < GT::R; ++q) v[q] = make_double2(0.0, 0.0);
   __syncthreads();
 
-  const bool pqs_on = (a.kf.mode & KM_PQS) != 0;
+  constexpr bool PQS = MODE >= 6;   // p̂·q̂ of the 2D body from the spectra
   __shared__ double s_pq[32];
   double pq_part = 0.0;
   // 4. T̃ via the circulant embedding (μ_s carries d or e, 1/L and 1/(2m))
@@ -295,15 +255,15 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
 #pragma unroll
   for (int q = 0; q < GT::R; ++q) {
     const double2 mq = a.mu[q * GT::P + t];  // lane-major table
-    // KM_PQS: p·(this pass's operator p) = Σ_k Re μ_k |Z_k|² over the packed
-    // pair (Parseval for the unnormalised forward/inverse pair and the real
+    // p·(this pass's operator p) = Σ_k Re μ_k |Z_k|² over the packed pair
+    // (Parseval for the unnormalised forward/inverse pair and the real
     // circulant; the zero padding makes the full-length sum the n-element dot).
     // Re(conj Z · μZ) = Re μ |Z|², taken from the product (no extra live values)
     const double2 z = v[q];
     v[q] = c_mul(z, mq);
-    if (pqs_on) pq_part = fma(z.x, v[q].x, fma(z.y, v[q].y, pq_part));
+    if (PQS) pq_part = fma(z.x, v[q].x, fma(z.y, v[q].y, pq_part));
   }
-  if (pqs_on) {  // park the warp's share in shared memory (nothing stays live through DST #2)
+  if (PQS) {  // park the warp's share in shared memory (nothing stays live through DST #2)
     pq_part = warp_sum(pq_part);
     if ((threadIdx.x & 31) == 0) s_pq[threadIdx.x >> 5] = pq_part;
   }
@@ -324,34 +284,7 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
 
   FDE_PROBE(4);
   // 6. epilogue
-  if (MODE == 4) {
-    // columns, recurrence body: w = ν ẑ + yin + op, q̂ = w + β q̂, p̂ = ẑ + β p̂
-    if (a.yin) cp_async_wait_all();
-    const double b4 = sst->betac;
-#pragma unroll
-    for (int i = 0; i < RD; ++i) {
-      const int e = RD * t + i - 1;
-      if (e < 0) continue;
-      if (v0) {
-        const long long o = A0.base + (long long)e * A0.stride;
-        const double z = a.kf.r[o] * fast_rcp(symbol_at<COL>(a, l0, e));
-        const double w = fma(a.nu, z, g0[i] + (a.yin ? smW[GD::swz(e)].x : 0.0));
-        const double qv = fma(b4, a.y[o], w), pv = fma(b4, a.kf.p[o], z);
-        a.y[o] = qv;
-        a.kf.p[o] = pv;
-        acc[0] = fma(pv, qv, acc[0]);
-      }
-      if (v1) {
-        const long long o = A1.base + (long long)e * A1.stride;
-        const double z = a.kf.r[o] * fast_rcp(symbol_at<COL>(a, l1, e));
-        const double w = fma(a.nu, z, g1[i] + (a.yin ? smW[GD::swz(e)].y : 0.0));
-        const double qv = fma(b4, a.y[o], w), pv = fma(b4, a.kf.p[o], z);
-        a.y[o] = qv;
-        a.kf.p[o] = pv;
-        acc[0] = fma(pv, qv, acc[0]);
-      }
-    }
-  } else if (MODE == 7) {  // columns of the concurrent body: w_c = op (one double2 per pair and row)
+  if (MODE == 7) {  // columns of the concurrent body: w_c = op (one double2 per pair and row)
 #pragma unroll
     for (int i = 0; i < RD; ++i) {
       const int e = RD * t + i - 1;
@@ -362,46 +295,6 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
       } else {
         if (v0) a.y[o0] = g0[i];
         if (v1) a.y[A1.base + (long long)e * A1.stride] = g1[i];
-      }
-    }
-  } else if (MODE == 1) {
-    // columns: this lane owns rows e = RD t + i - 1 of its two columns
-    if (FDE_SINE_YIN_ASYNC && a.yin) cp_async_wait_all();
-    const bool pqs = (a.kf.mode & KM_PQS) != 0;
-#pragma unroll
-    for (int i = 0; i < RD; ++i) {
-      const int e = RD * t + i - 1;
-      if (e < 0) continue;
-      if (pqs && vec2 && FDE_SINE_YIN_ASYNC) {  // q̂ = yin + op: p̂·q̂ came from the spectrum, ν is in the row pass
-        const long long o = A0.base + (long long)e * A0.stride;
-        const double2 yv = a.yin ? smW[GD::swz(e)] : make_double2(0.0, 0.0);
-        *reinterpret_cast<double2*>(a.y + o) = make_double2(g0[i] + yv.x, g1[i] + yv.y);
-        continue;
-      }
-      if (vec2 && FDE_SINE_YIN_ASYNC) {  // both columns of the pair as one double2
-        const long long o = A0.base + (long long)e * A0.stride;
-        const double2 pv = *reinterpret_cast<const double2*>(a.kf.p + o);
-        const double2 yv = a.yin ? smW[GD::swz(e)] : make_double2(0.0, 0.0);
-        const double2 qv = make_double2(fma(a.nu, pv.x, g0[i] + yv.x), fma(a.nu, pv.y, g1[i] + yv.y));
-        *reinterpret_cast<double2*>(a.y + o) = qv;
-        acc[0] = fma(pv.x, qv.x, fma(pv.y, qv.y, acc[0]));
-        continue;
-      }
-      if (v0) {
-        const long long o = A0.base + (long long)e * A0.stride;
-        const double pv = a.kf.p[o];
-        const double yv = a.yin ? (FDE_SINE_YIN_ASYNC ? smW[GD::swz(e)].x : a.yin[o]) : 0.0;
-        const double qv = fma(a.nu, pv, g0[i] + yv);
-        a.y[o] = qv;
-        if (!pqs) acc[0] = fma(pv, qv, acc[0]);
-      }
-      if (v1) {
-        const long long o = A1.base + (long long)e * A1.stride;
-        const double pv = a.kf.p[o];
-        const double yv = a.yin ? (FDE_SINE_YIN_ASYNC ? smW[GD::swz(e)].y : a.yin[o]) : 0.0;
-        const double qv = fma(a.nu, pv, g1[i] + yv);
-        a.y[o] = qv;
-        if (!pqs) acc[0] = fma(pv, qv, acc[0]);
       }
     }
   } else {
@@ -417,10 +310,10 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
       if (e >= n) continue;
       const double2 o = sm[GD::swz(e)];
       const long long o0 = A0.base + (long long)e * A0.stride, o1 = A1.base + (long long)e * A1.stride;
-      if (MODE == 0 || MODE == 3 || MODE == 6) {
+      if (MODE == 6) {
         if (v0) a.y[o0] = o.x;
         if (v1) a.y[o1] = o.y;
-      } else if (MODE == 5) {  // 1D recurrence body: q̂ = ν ẑ + (S T̃ S) ẑ + β q̂, p̂ = ẑ + β p̂
+      } else {  // MODE 5 (1D recurrence body): q̂ = ν ẑ + (S T̃ S) ẑ + β q̂, p̂ = ẑ + β p̂
         if (v0) {
           const double z = a.kf.r[o0] * fast_rcp(symbol_at<COL>(a, l0, e));
           const double qv = fma(beta5, a.y[o0], fma(a.nu, z, o.x)), pv = fma(beta5, a.kf.p[o0], z);
@@ -435,21 +328,10 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
           a.kf.p[o1] = pv;
           acc[0] = fma(pv, qv, acc[0]);
         }
-      } else {  // 1D: q̂ = ν p̂ + (S T̃ S) p̂, p̂·q̂
-        if (v0) {
-          const double pv = a.kf.p[o0], qv = fma(a.nu, pv, o.x);
-          a.y[o0] = qv;
-          acc[0] = fma(pv, qv, acc[0]);
-        }
-        if (v1) {
-          const double pv = a.kf.p[o1], qv = fma(a.nu, pv, o.y);
-          a.y[o1] = qv;
-          acc[0] = fma(pv, qv, acc[0]);
-        }
       }
     }
   }
-  if ((MODE == 0 || MODE == 1 || MODE >= 6) && pqs_on) acc[0] += (threadIdx.x & 31) == 0 ? s_pq[threadIdx.x >> 5] : 0.0;
+  if (PQS) acc[0] += (threadIdx.x & 31) == 0 ? s_pq[threadIdx.x >> 5] : 0.0;
   if (MODE == 5) {  // α_k = ρ_k / (p̂·q̂) inside the CTA
     acc[1] = acc[2] = 0.0;
     block_reduce3(acc, scr);
@@ -469,12 +351,7 @@ __device__ __forceinline__ void sineop_body(const LineArgs& a, const int bx) {
     }
     __syncthreads();
     if (s_stop5) break;
-  } else if (MODE == 0 && (a.kf.mode & KM_PQX)) {  // the row pass's share of p̂·q̂, finalised by the column pass
-    block_reduce3(acc, scr);
-    if (threadIdx.x == 0) a.kf.part[(size_t)blockIdx.y * 3 * KPMAX + KPMAX / 2 + blockIdx.x] = acc[0];
-  } else if (MODE == 1 || MODE == 2 || MODE == 4 || MODE >= 6) {
-    kry_reduce_finalize(a.kf, acc);
-  } else if (MODE == 3) {
+  } else {
     kry_reduce_finalize(a.kf, acc);
   }
   FDE_PROBE(5);
@@ -526,159 +403,6 @@ k_sineop_rc(LineArgs ar, LineArgs ac, int gc) {
     }                                                                             \
   }
 
-// PCG vector step in the sine domain: x̂ += α p̂, r̂ -= α q̂, partials ‖r̂‖² and
-// r̂·ẑ = Σ r̂²/F (the diagonal preconditioner), finalised like KM_XR | KM_RZ.
-// 2D: a block per row (strided over rows); every thread issues the loads of
-// its XR_U elements of the row before any arithmetic (loads in flight).
-constexpr int XR_U = 4;
-__global__ void __launch_bounds__(256) k_sine_xr(KryFuse k, int n, int dims, const double* __restrict__ Fx,
-                                                 const double* __restrict__ Fy, int pitch) {
-  FDE_PDL_ENTRY();
-  const int rhs = blockIdx.y;
-  if (!k.st[rhs].cyc_active) return;
-  const size_t o = (size_t)rhs * (dims == 2 ? (size_t)n * pitch : (size_t)n);
-  const double al = k.st[rhs].alpha;
-  double* __restrict__ xr = k.x + o;
-  double* __restrict__ rr = k.r + o;
-  const double* __restrict__ pr = k.p + o;
-  const double* __restrict__ qr = k.q + o;
-  double acc[3] = {0.0, 0.0, 0.0};
-  const int rows = dims == 2 ? n : 1;
-  for (int j = blockIdx.x; j < rows; j += gridDim.x) {
-    const double fy = dims == 2 ? Fy[j] : 0.0;
-    const size_t rb = (size_t)j * (dims == 2 ? pitch : n);
-    for (int i0 = threadIdx.x; i0 < n; i0 += XR_U * blockDim.x) {
-      double qv[XR_U], rv[XR_U], pv[XR_U], xv[XR_U], fv[XR_U];
-#pragma unroll
-      for (int u = 0; u < XR_U; ++u) {
-        const int i = i0 + u * blockDim.x;
-        const bool ok = i < n;
-        qv[u] = ok ? qr[rb + i] : 0.0;
-        rv[u] = ok ? rr[rb + i] : 0.0;
-        pv[u] = ok ? pr[rb + i] : 0.0;
-        xv[u] = ok ? xr[rb + i] : 0.0;
-        fv[u] = ok ? Fx[i] + fy : 1.0;
-      }
-#pragma unroll
-      for (int u = 0; u < XR_U; ++u) {
-        const int i = i0 + u * blockDim.x;
-        const double r = fma(-al, qv[u], rv[u]);
-        if (i < n) {
-          rr[rb + i] = r;
-          xr[rb + i] = fma(al, pv[u], xv[u]);
-        }
-        acc[1] = fma(r, r, acc[1]);
-        acc[2] = fma(r * r, fast_rcp(fv[u]), acc[2]);
-      }
-    }
-  }
-  kry_reduce_finalize(k, acc);
-}
-
-// 2D vector step over the internal layout (n rows of pitch 2^lgp >= n+1) as a
-// flat array of 16-byte pairs: no per-row loop, every thread issues the loads
-// of its XR2_U pairs before any arithmetic. The padding entries i >= n of
-// every row are zero in r̂, q̂, p̂, x̂ (k_sine_init) and stay zero here.
-#ifndef FDE_XR2_U
-#define FDE_XR2_U 2
-#endif
-constexpr int XR2_U = FDE_XR2_U;
-__global__ void __launch_bounds__(256) k_sine_xr2(KryFuse k, int n, int lgp, const double* __restrict__ Fx,
-                                                  const double* __restrict__ Fy) {
-  FDE_PDL_ENTRY();
-  const int rhs = blockIdx.y;
-  if (!k.st[rhs].cyc_active) return;
-  const int pitch = 1 << lgp;
-  const size_t o = (size_t)rhs * ((size_t)n << lgp);
-  const int npairs = (n << lgp) >> 1;
-  const double al = k.st[rhs].alpha;
-  double2* __restrict__ xr = reinterpret_cast<double2*>(k.x + o);
-  double2* __restrict__ rr = reinterpret_cast<double2*>(k.r + o);
-  const double2* __restrict__ pr = reinterpret_cast<const double2*>(k.p + o);
-  const double2* __restrict__ qr = reinterpret_cast<const double2*>(k.q + o);
-  const int T = gridDim.x * blockDim.x;
-  double acc[3] = {0.0, 0.0, 0.0};
-  for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < npairs; c0 += XR2_U * T) {
-    double2 qv[XR2_U], rv[XR2_U], pv[XR2_U], xv[XR2_U], fv[XR2_U];
-#pragma unroll
-    for (int u = 0; u < XR2_U; ++u) {
-      const int c = c0 + u * T;
-      const bool ok = c < npairs;
-      const double2 z = make_double2(0.0, 0.0);
-      qv[u] = ok ? qr[c] : z;
-      rv[u] = ok ? rr[c] : z;
-      pv[u] = ok ? pr[c] : z;
-      xv[u] = ok ? xr[c] : z;
-      const int e = 2 * c, j = e >> lgp, i = e & (pitch - 1);
-      const double fy = ok ? Fy[j] : 0.0;
-      fv[u] = make_double2(ok && i < n ? Fx[i] + fy : 1.0, ok && i + 1 < n ? Fx[i + 1] + fy : 1.0);
-    }
-#pragma unroll
-    for (int u = 0; u < XR2_U; ++u) {
-      const int c = c0 + u * T;
-      const double2 r = make_double2(fma(-al, qv[u].x, rv[u].x), fma(-al, qv[u].y, rv[u].y));
-      if (c < npairs) {
-        rr[c] = r;
-        xr[c] = make_double2(fma(al, pv[u].x, xv[u].x), fma(al, pv[u].y, xv[u].y));
-      }
-      acc[1] = fma(r.x, r.x, fma(r.y, r.y, acc[1]));
-      acc[2] = fma(r.x * r.x, fast_rcp(fv[u].x), fma(r.y * r.y, fast_rcp(fv[u].y), acc[2]));
-    }
-  }
-  kry_reduce_finalize(k, acc);
-}
-
-// vector step of the concurrent body (after k_sineop_rc, whose row units wrote
-// p̂_new and applied the lagged x̂ += α_{k-1} p̂_{k-1}): q̂ = w_r + w_c,
-// r̂ -= α q̂, partials ‖r̂‖², r̂·ẑ (k_sine_xfix adds the last α p̂ after the
-// loop). Flat over the internal layout like k_sine_xr2; padding entries
-// (i >= n) of w_r, w_c are never written, so they are masked here.
-__global__ void __launch_bounds__(256, 4) k_sine_xr3(KryFuse k, int n, int lgp, const double* __restrict__ Fx,
-                                                  const double* __restrict__ Fy, const double* __restrict__ wr_,
-                                                  const double* __restrict__ wc_) {
-  FDE_PDL_ENTRY();
-  const int rhs = blockIdx.y;
-  if (!k.st[rhs].cyc_active) return;
-  const int pitch = 1 << lgp;
-  const size_t o = (size_t)rhs * ((size_t)n << lgp);
-  const int npairs = (n << lgp) >> 1;
-  const double al = k.st[rhs].alpha;
-  double2* __restrict__ rr = reinterpret_cast<double2*>(k.r + o);
-  const double2* __restrict__ wr = reinterpret_cast<const double2*>(wr_ + o);
-  const double2* __restrict__ wc = reinterpret_cast<const double2*>(wc_ + o);
-  const int T = gridDim.x * blockDim.x;
-  double acc[3] = {0.0, 0.0, 0.0};
-  for (int c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < npairs; c0 += XR2_U * T) {
-    double2 rv[XR2_U], av[XR2_U], bv[XR2_U], fv[XR2_U];
-    bool okx[XR2_U], oky[XR2_U];
-#pragma unroll
-    for (int u = 0; u < XR2_U; ++u) {
-      const int c = c0 + u * T;
-      const bool ok = c < npairs;
-      const double2 z = make_double2(0.0, 0.0);
-      rv[u] = ok ? rr[c] : z;
-      av[u] = ok ? wr[c] : z;
-      bv[u] = ok ? wc[c] : z;
-      const int e = 2 * c, j = e >> lgp, i = e & (pitch - 1);
-      const double fy = ok ? Fy[j] : 0.0;
-      okx[u] = ok && i < n;
-      oky[u] = ok && i + 1 < n;
-      fv[u] = make_double2(okx[u] ? Fx[i] + fy : 1.0, oky[u] ? Fx[i + 1] + fy : 1.0);
-    }
-#pragma unroll
-    for (int u = 0; u < XR2_U; ++u) {
-      const int c = c0 + u * T;
-      const double2 iF = make_double2(fast_rcp(fv[u].x), fast_rcp(fv[u].y));
-      const double2 q = make_double2(okx[u] ? av[u].x + bv[u].x : 0.0, oky[u] ? av[u].y + bv[u].y : 0.0);
-      const double2 r = make_double2(fma(-al, q.x, rv[u].x), fma(-al, q.y, rv[u].y));
-      if (c < npairs) rr[c] = r;
-      acc[1] = fma(r.x, r.x, fma(r.y, r.y, acc[1]));
-      acc[2] = fma(r.x * r.x, iF.x, fma(r.y * r.y, iF.y, acc[2]));
-    }
-  }
-  kry_reduce_finalize(k, acc);
-}
-
 // 32-byte accesses (sm_100 LDG.E.256 / STG.E.256)
 struct alignas(32) dbl4 {
   double x, y, z, w;
@@ -692,7 +416,12 @@ __device__ __forceinline__ void st4(double* p, const dbl4& v) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
 }
 
-// k_sine_xr3 over 32-byte groups of 4 elements (pitch a multiple of 4)
+// vector step of the concurrent body (after k_sineop_rc, whose row units wrote
+// p̂_new and applied the lagged x̂ += α_{k-1} p̂_{k-1}): q̂ = w_r + w_c,
+// r̂ -= α q̂, partials ‖r̂‖², r̂·ẑ (k_sine_xfix adds the last α p̂ after the
+// loop), over 32-byte groups of 4 elements of the internal layout (pitch a
+// multiple of 4; the padding entries i >= n of w_r, w_c are never written,
+// so they are masked here)
 #ifndef FDE_XR4_U
 #define FDE_XR4_U 1
 #endif

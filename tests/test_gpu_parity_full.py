@@ -5,7 +5,7 @@ reproduced with every solve on the GPU.
 
 What these check is τ and S applied through eq:tau and eq:sine_transform
  inside the production launch configuration: cfg 5 at n = 1023 is
-the bench workload (the concurrent sine-domain body), n = 2047 the second
+the bench workload (the r02 sine-domain body), n = 2047 the second
 north_star size, cfg 4 at n = 1023 the GMRES(30) workload. The oracle's dense
 products cost ~17 GFlop per iteration at n = 1023, so each oracle solve runs
 once per module (cached) and is shared by the GPU variants.
@@ -76,7 +76,7 @@ def check(stats, x, p, s, res):
 
 
 # the sine-domain PCG body variants the library can run at these sizes
-PCG_BODIES = [{}, {"FDE_SINE_RC": "0"}, {"FDE_SINE_RC": "1"}]
+PCG_BODIES = [{}, {"FDE_SOP": "0"}]   # the r02 body (default) and the r01 concurrent body
 
 
 @pytest.mark.parametrize("env", PCG_BODIES, ids=lambda e: ",".join("%s=%s" % kv for kv in e.items()) or "default")

@@ -78,14 +78,13 @@ def test_solver_parity(torch_cuda, cfg, n, batch, solver, prec):
         assert np.linalg.norm(r) / np.linalg.norm(p.rhs[b]) <= 1e-9
 
 
-@pytest.mark.parametrize("orth,ws", [("dcgs2", "1"), ("cgs2", "1"), ("cgs2", "0")])
-def test_gmres_cgs_kernel_variants(torch_cuda, monkeypatch, orth, ws):
-    """Every orthogonalisation path matches the oracle's GMRES(30) (CGS2):
-    DCGS2 (the default for restart <= 31: delayed reorthogonalisation, two
-    passes over the basis per step), and CGS2 with warp-split (FDE_GM_WS=1) or
-    one-thread-per-element (0) kernels."""
+@pytest.mark.parametrize("orth", ["dcgs2", "cgs2"])
+def test_gmres_cgs_kernel_variants(torch_cuda, monkeypatch, orth):
+    """Both orthogonalisations match the oracle's GMRES(30) (CGS2): DCGS2 (the
+    default for restart <= 31: delayed reorthogonalisation, two passes over
+    the basis per step) and CGS2 (FDE_GM_ORTH=cgs2: warp-split passes for
+    j < 32, one thread per element beyond)."""
     monkeypatch.setenv("FDE_GM_ORTH", orth)
-    monkeypatch.setenv("FDE_GM_WS", ws)
     for cfg, n, batch, prec in ((2, 255, 2, W.PREC_TAU_D), (4, 127, 1, W.PREC_TAU)):
         p = W.config(cfg, n=n, batch=batch, prec=prec)
         s = oracle_system(p)
@@ -94,8 +93,8 @@ def test_gmres_cgs_kernel_variants(torch_cuda, monkeypatch, orth, ws):
         for b in range(batch):
             xo, it_o, conv_o, _ = ref[b]
             assert stats[b]["converged"] and conv_o
-            assert abs(stats[b]["iters"] - it_o) <= 1, (orth, ws, b, stats[b]["iters"], it_o)
-            assert relerr(x[b], xo) <= 1e-9, (orth, ws, relerr(x[b], xo))
+            assert abs(stats[b]["iters"] - it_o) <= 1, (orth, b, stats[b]["iters"], it_o)
+            assert relerr(x[b], xo) <= 1e-9, (orth, relerr(x[b], xo))
 
 
 def test_gmres_left_unrestarted_matches_oracle(torch_cuda):
@@ -153,20 +152,17 @@ def _solve_with_env(torch, p, env):
     return stats, out
 
 
-@pytest.mark.parametrize("cfg,n,batch", [(1, 127, 2), (3, 63, 1), (5, 255, 3), (3, 511, 1)])
+@pytest.mark.parametrize("cfg,n,batch", [(1, 127, 2), (3, 63, 1), (5, 255, 3), (3, 511, 1), (5, 511, 2)])
 def test_pcg_sine_domain_and_standard_paths_agree_with_oracle(torch_cuda, cfg, n, batch):
     """Constant coefficients + τ: fde_pcg runs PCG in the sine basis (DESIGN.md
-    §5.4; FDE_SINE_BODY=2 selects its recurrence body, FDE_SINE_PQ=direct the
-    elementwise p̂·q̂ instead of the spectral one, FDE_SINE_XR=rows the per-row
-    vector step, FDE_SINE_RC=0 the two-pass body instead of the concurrent one); FDE_PCG=standard forces the standard-domain fused iteration.
-    All must match the oracle's PCG (iterations ±1, solution 1e-9)."""
+    §5.4): the r02 body (sop_kernels.cuh) for n+1 in {512..4096}, FDE_SOP=0
+    the r01 concurrent body; FDE_PCG=standard forces the standard-domain
+    fused iteration. All must match the oracle's PCG (iterations ±1,
+    solution 1e-9)."""
     p = W.config(cfg, n=n, batch=batch)
     s = oracle_system(p)
     ref = oracle_solve(p, s, "pcg")
-    for env in ({}, {"FDE_SINE_BODY": "2"}, {"FDE_PCG": "standard"}, {"FDE_SINE1D": "graph"},
-                {"FDE_SINE_RC": "0"}, {"FDE_SINE_RC": "1"}, {"FDE_SINE_RC": "1", "FDE_XR4": "0"},
-                {"FDE_SINE_RC": "0", "FDE_SINE_PQ": "direct"},
-                {"FDE_SINE_RC": "0", "FDE_SINE_XR": "rows"}):
+    for env in ({}, {"FDE_PCG": "standard"}, {"FDE_SOP": "0"}):
         stats, x = _solve_with_env(torch_cuda, p, env)
         for b in range(batch):
             xo, it_o, conv_o, _ = ref[b]
@@ -189,15 +185,14 @@ def test_pcg_variable_coefficients_standard_path(torch_cuda):
     assert relerr(x[0], xo) <= 1e-9
 
 
-@pytest.mark.parametrize("body", ["0", "1"])
-def test_batch_rhs_are_independent_and_deterministic(torch_cuda, monkeypatch, body):
+@pytest.mark.parametrize("sop", ["1", "0"])
+def test_batch_rhs_are_independent_and_deterministic(torch_cuda, monkeypatch, sop):
     """Per-RHS grids and per-RHS fixed-order reductions: a batch-3 solve equals
     the three single-RHS solves bitwise, and repeating a solve is bitwise
-    identical. The 2D sine-domain body is picked by (batch, n) by
-    default, so it is pinned here (FDE_SINE_RC) for both."""
+    identical; for both 2D sine-domain bodies (FDE_SOP) and GMRES."""
     from paper_1912_13304_b200 import fde
-    monkeypatch.setenv("FDE_SINE_RC", body)
-    for cfg, n, solver in ((5, 255, "pcg"), (4, 127, "gmres")):
+    monkeypatch.setenv("FDE_SOP", sop)
+    for cfg, n, solver in ((5, 511, "pcg"), (5, 255, "pcg"), (4, 127, "gmres")):
         p = W.config(cfg, n=n, batch=3)
         _, _, x3, _ = gpu_solve(torch_cuda, p, solver)
         _, _, x3b, _ = gpu_solve(torch_cuda, p, solver)
@@ -361,19 +356,19 @@ def test_orders_near_the_bounds(torch_cuda, alpha, beta):
     assert abs(stats[0]["iters"] - it_o) <= 1 and relerr(x[0], xo) <= 1e-9
 
 
-@pytest.mark.parametrize("cfg,n,batch,solver,rc", [(5, 4095, 2, "pcg", None), (5, 2047, 8, "pcg", None),
-                                                   (5, 2047, 1, "pcg", None), (5, 4095, 1, "pcg", "1"),
-                                                   (5, 1023, 1, "pcg", None), (2, 4095, 2, "gmres", None),
-                                                   (4, 1023, 1, "gmres", None)])
-def test_full_size_solves_true_residual(torch_cuda, monkeypatch, cfg, n, batch, solver, rc):
+@pytest.mark.parametrize("cfg,n,batch,solver,sop", [(5, 4095, 2, "pcg", None), (5, 2047, 8, "pcg", None),
+                                                    (5, 2047, 1, "pcg", None), (5, 4095, 1, "pcg", "0"),
+                                                    (5, 1023, 8, "pcg", None), (2, 4095, 2, "gmres", None),
+                                                    (4, 1023, 1, "gmres", None)])
+def test_full_size_solves_true_residual(torch_cuda, monkeypatch, cfg, n, batch, solver, sop):
     """Largest sizes/batches the bench sweep runs (the oracle's full solves at
     n = 1023 and 2047 are in test_gpu_parity_full.py): check what holds at any
     size — the true residual ‖b - A x‖/‖b‖ per RHS, with A applied by the
     ORACLE's dense matvec (O.System.matvec, one RHS at a time) — meets the
     tolerance."""
     from paper_1912_13304_b200 import fde
-    if rc is not None:  # the concurrent sine body also at n = 4095 (by default only n <= 2047)
-        monkeypatch.setenv("FDE_SINE_RC", rc)
+    if sop is not None:  # the r01 concurrent body at n = 4095 (by default the r02 body)
+        monkeypatch.setenv("FDE_SOP", sop)
     p = W.config(cfg, n=n, batch=batch)
     h = fde.Fde.from_problem(p)
     b = torch_cuda.from_numpy(p.rhs.copy()).cuda()
