@@ -385,9 +385,11 @@ __device__ __forceinline__ void transform(double2 (&v)[16], double2* sm, int t, 
 // one full 32-byte sector per row, through L1) was slower than one
 template <int U>
 __host__ __device__ constexpr int sop_upc() { return 1; }
-// registers per thread: 7 units of m = 1024 (14 warps) resident per SM
+// registers per thread (measured): m = 1024: 144 (7 units = 14 warps per SM);
+// m = 2048: 168 (3 units, 12 warps: no spills, 4% faster than 128 with
+// spills); m = 4096: 128 (2 units; 168 leaves one unit per SM, 10% slower)
 template <int U>
-__host__ __device__ constexpr int sop_maxreg() { return U <= 32 ? 168 : U == 64 ? 144 : 128; }
+__host__ __device__ constexpr int sop_maxreg() { return U <= 32 ? 168 : U == 64 ? 144 : U == 128 ? 168 : 128; }
 
 // One launch = the even part of both directions' operators for every active
 // RHS: CTA b holds units upc·b + s (s < upc); column units first.
