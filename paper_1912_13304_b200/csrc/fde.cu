@@ -1332,8 +1332,8 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     sa.p2 = h->kp2;
     sa.wr = h->wx;
     sa.wc = h->wy;
-    sa.hx = h->sop_hx;
-    sa.hy = h->sop_hy;
+    sa.nu = h->d.nu;
+    sa.lscale = 4.0 * (double)h->m * (double)h->m;
     sa.mux = h->sop_mux;
     sa.muy = h->sop_muy;
     sa.tw = h->sop_tw;

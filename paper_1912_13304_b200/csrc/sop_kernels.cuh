@@ -49,8 +49,8 @@ struct SopArgs {
   double* p2;                 // p̂ buffer 1 (SolveState::ppar names the p̂_old buffer)
   double* wr;                 // row-direction output (even part)
   double* wc;                 // column-direction output (even part)
-  const double* hx;           // ν + ½λ^α_{i+1}: the diagonal of the row direction
-  const double* hy;           // ½λ^β_{j+1}
+  double nu;                  // ν
+  double lscale;              // 4m²: ½λ_k = 4m²·μ'_k (the diagonal from the μ' tables, no extra table)
   const double* mux;          // μ'_k = λ^α_k/(8m²), k = 0..m (row direction)
   const double* muy;          // μ'_k = λ^β_k/(8m²) (column direction)
   const double2* tw;          // ω_m^e = exp(-2πi e/m), e < m/2
@@ -446,7 +446,8 @@ __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>())
     }
   } else {
     const size_t o0 = base + (size_t)l0 * pitch, o1 = base + (size_t)(v1 ? l1 : l0) * pitch;
-    const double hy0 = __ldg(a.hy + l0), hy1 = v1 ? __ldg(a.hy + l1) : 0.0;
+    // diagonal ν + ½λ^α_{i+1} + ½λ^β_{j+1} from the μ' tables (½λ_k = 4m² μ'_k)
+    const double hy0 = a.lscale * __ldg(a.muy + l0 + 1), hy1 = v1 ? a.lscale * __ldg(a.muy + l1 + 1) : 0.0;
     const double alpha = st.alpha;
 #pragma unroll
     for (int c = 0; c < 16; c += 4) {
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>())
       for (int i = 0; i < 4; ++i) {
         const int j = t + U * (c + i);
         const int e = j >= 1 ? j - 1 : 0;
-        const double hx = __ldg(a.hx + e);
+        const double hx = fma(a.lscale, __ldg(a.mux + e + 1), a.nu);
         const double p0 = fma(beta, q0[i], z0[i]);
         const double p1 = v1 ? fma(beta, q1[i], z1[i]) : 0.0;
         if (j >= 1) {
