@@ -1173,10 +1173,18 @@ void ensure_krylov(fde_handle h, int nvecV) {
 
 #define VGRID dim3(RED_BLOCKS, h->batch)
 
-// Build `*out` = [WHILE(cond) { body() ; k_loop_ctrl }] by capturing body()
-// into the conditional node's body graph. Returns the kernel nodes per body.
+// Build `*out` = [WHILE(cond) { body() × unroll ; k_loop_ctrl }] by capturing
+// body() into the conditional node's body graph. Returns the kernel nodes per
+// loop body. Every kernel of a body is a no-op for finished RHS (per-RHS
+// gates), so the `unroll` copies after convergence cost only their empty
+// launches, while the WHILE node's per-body re-evaluation (≈8 µs measured on
+// the B200 between k_loop_ctrl and the next body's first kernel) is paid once
+// per `unroll` iterations.
+#ifndef FDE_PCG_UNROLL
+#define FDE_PCG_UNROLL 4
+#endif
 template <class F>
-int build_while_graph(fde_handle h, cudaGraphExec_t* out, int maxloops, F&& body) {
+int build_while_graph(fde_handle h, cudaGraphExec_t* out, int maxloops, F&& body, int unroll = 1) {
   cudaGraph_t g;
   FDE_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle ch;
@@ -1196,8 +1204,8 @@ int build_while_graph(fde_handle h, cudaGraphExec_t* out, int maxloops, F&& body
   h->st = cs;
   try {
     FDE_CUDA(cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    body();
-    launch_k(cs, k_loop_ctrl, 1, 1, 0, ch, h->ctr, maxloops);
+    for (int u = 0; u < unroll; ++u) body();
+    launch_k(cs, k_loop_ctrl, 1, 1, 0, ch, h->ctr, unroll == 1 ? maxloops : (maxloops + unroll - 1) / unroll + 1);
     FDE_CUDA(cudaGetLastError());
     cudaGraph_t captured;
     FDE_CUDA(cudaStreamEndCapture(cs, &captured));
@@ -1301,6 +1309,31 @@ void op_dst_all(fde_handle h, const double* x, double* y, double oscale) {
 // the vector step adding the diagonal) for n+1 in {512..4096}, else the r01
 // concurrent body (k_sineop_rc + k_sine_xr4).
 constexpr int XR_GRID = 592;   // CTAs of the sine-domain vector steps (4 per SM)
+fde::sop::SopArgs sop_args(fde_handle h) {
+  fde::sop::SopArgs sa{};
+  sa.n = h->n;
+  sa.m = h->m;
+  sa.pitch = h->sine_pitch;
+  sa.npairs = h->m / 2;
+  sa.total_warps = fde::sop::warps_for(h->m, h->batch);
+  sa.z = h->kq;   // ẑ = r̂/F (k_sine_init / k_sine_xr5)
+  sa.x = h->kx;
+  sa.p = h->kp;
+  sa.p2 = h->kp2;
+  sa.wr = h->wx;
+  sa.wc = h->wy;
+  sa.nu = h->d.nu;
+  sa.lscale = 4.0 * (double)h->m * (double)h->m;
+  sa.mux = h->sop_mux;
+  sa.muy = h->sop_muy;
+  sa.tw = h->sop_tw;
+  sa.sc = h->sop_sc;
+  sa.st = h->sst;
+  sa.ctr = h->ctr;
+  sa.part = h->spart;
+  return sa;
+}
+
 void sine_iteration(fde_handle h, double rtol, int maxit) {
   KryFuse kf = make_kf(h, rtol, maxit);
   LineArgs a = base_args(h);
@@ -1320,27 +1353,7 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
   while ((1 << lgp) < h->sine_pitch) ++lgp;
   if ((1 << lgp) != h->sine_pitch || lgp < 2) throw FdeFail{FDE_ERR_UNSUPPORTED, "sine pitch is not a power of two"};
   if (h->sop_ok) {
-    fde::sop::SopArgs sa{};
-    sa.n = h->n;
-    sa.m = h->m;
-    sa.pitch = h->sine_pitch;
-    sa.npairs = h->m / 2;
-    sa.total_warps = fde::sop::warps_for(h->m, h->batch);
-    sa.z = h->kq;   // ẑ = r̂/F (k_sine_init / k_sine_xr5)
-    sa.x = h->kx;
-    sa.p = h->kp;
-    sa.p2 = h->kp2;
-    sa.wr = h->wx;
-    sa.wc = h->wy;
-    sa.nu = h->d.nu;
-    sa.lscale = 4.0 * (double)h->m * (double)h->m;
-    sa.mux = h->sop_mux;
-    sa.muy = h->sop_muy;
-    sa.tw = h->sop_tw;
-    sa.sc = h->sop_sc;
-    sa.st = h->sst;
-    sa.ctr = h->ctr;
-    sa.part = h->spart;
+    const fde::sop::SopArgs sa = sop_args(h);
     launch_named(h, "sine_op_sop", [&] { FDE_CUDA(fde::sop::launch(sa, h->st)); });
     KryFuse kv = kf;
     kv.mode = KM_XR | KM_RZ | KM_GATE;
@@ -1410,7 +1423,7 @@ fde_status run_pcg_sine(fde_handle h, const double* b, double* x, double rtol, i
     FDE_SWITCH_K(h->K, (launch_sineop_k<KK - 1, false, 5>(h, a)));
   } else if (!h->no_graph && (!h->g_pcg || h->g_pcg_kind != 1 || h->g_pcg_rtol != rtol || h->g_pcg_maxit != maxit)) {
     if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
-    h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { sine_iteration(h, rtol, maxit); });
+    h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { sine_iteration(h, rtol, maxit); }, FDE_PCG_UNROLL);
     h->g_pcg_kind = 1;
     h->g_pcg_rtol = rtol;
     h->g_pcg_maxit = maxit;
@@ -1467,7 +1480,7 @@ fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int ma
   // whose body is one PCG iteration plus k_loop_ctrl (no host round trips)
   if (!h->g_pcg || h->g_pcg_kind != 0 || h->g_pcg_rtol != rtol || h->g_pcg_maxit != maxit) {
     if (h->g_pcg) { cudaGraphExecDestroy(h->g_pcg); h->g_pcg = nullptr; }
-    h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { pcg_iteration(h, va); });
+    h->g_pcg_nodes = build_while_graph(h, &h->g_pcg, maxit + 1, [&] { pcg_iteration(h, va); }, FDE_PCG_UNROLL);
     h->g_pcg_kind = 0;
     h->g_pcg_rtol = rtol;
     h->g_pcg_maxit = maxit;
@@ -1952,3 +1965,12 @@ fde_status fde_profile_unit(fde_handle h, const double* x, double* y, double* z,
 }
 
 }  // extern "C"
+
+#if FDE_SOP_TRACE
+// measurement builds only (-DFDE_SOP_TRACE=1): k_sine_xr5 CTA start/end and
+// the loop control's time of the last iteration
+extern "C" int fde_debug_xr_trace(unsigned long long* host, int n) {
+  if (n > 4096) n = 4096;
+  return (int)cudaMemcpyFromSymbol(host, fde::g_xr_trace, sizeof(unsigned long long) * n);
+}
+#endif

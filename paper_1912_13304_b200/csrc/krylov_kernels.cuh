@@ -1046,12 +1046,27 @@ __global__ void k_pcg_xrz_none(KryFuse k, int N, double* __restrict__ z) {
   kry_reduce_finalize(k, acc);
 }
 
+#ifndef FDE_SOP_TRACE
+#define FDE_SOP_TRACE 0   // measurement builds only (timeline of the sine body)
+#endif
+#if FDE_SOP_TRACE
+__device__ unsigned long long g_xr_trace[4096];   // [cta][start, end]; [2048] = loop_ctrl
+__device__ __forceinline__ unsigned long long xr_gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#endif
+
 // while-loop control of a CUDA graph (conditional WHILE node): keep looping
 // while some RHS is still iterating, at most maxloops bodies.
 __global__ void k_loop_ctrl(cudaGraphConditionalHandle hdl, Counters* c, int maxloops) {
   FDE_PDL_ENTRY();
   const int loops = c->loops + 1;
   c->loops = loops;
+#if FDE_SOP_TRACE
+  g_xr_trace[2048] = xr_gtime();
+#endif
   cudaGraphSetConditional(hdl, (c->active > 0 && loops < maxloops) ? 1u : 0u);
 }
 

@@ -57,6 +57,16 @@ struct Counters {            // device counters
   unsigned tickets[64];      // per-RHS last-block tickets (batch <= 8, 8 slots each)
 };
 
+// 1/x to ~1 ulp for 1e-30 < x < 1e30: fp32 seed + two Newton steps (FP64 FMA),
+// avoiding the IEEE division slow path inside the transform kernels.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r = (double)__frcp_rn((float)x);
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

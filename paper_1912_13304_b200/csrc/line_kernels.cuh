@@ -103,15 +103,6 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// 1/x to ~1 ulp for 1e-30 < x < 1e30: fp32 seed + two Newton steps (FP64 FMA),
-// avoiding the IEEE division slow path inside the transform kernels.
-__device__ __forceinline__ double fast_rcp(double x) {
-  double r = (double)__frcp_rn((float)x);
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 // Threads per CTA x resident CTAs per SM = 512: caps registers at 128 so that
 // all line pairs of an n = 1023 pass are resident in one wave.

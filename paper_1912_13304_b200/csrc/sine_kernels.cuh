@@ -494,6 +494,9 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
                                                      int nsp) {
   FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
+#if FDE_SOP_TRACE
+  if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 2] = xr_gtime();
+#endif
   if (!k.st[rhs].cyc_active) return;
   __shared__ double s_pq[8];
   {
@@ -551,6 +554,9 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
   kk.mode = k.mode | KM_SOPA;
   kk.xval = pq;   // every CTA summed the same partials in the same order: the finaliser's α is this CTA's α
   kry_reduce_finalize(kk, acc);
+#if FDE_SOP_TRACE
+  if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 2 + 1] = xr_gtime();
+#endif
 }
 
 // end of a concurrent-body solve: the lagged x̂ += α p̂ of the last iteration

@@ -35,3 +35,11 @@ int warps_for(int m, int batch) { return batch * m; }   // units (CTAs): 2·npai
 
 }  // namespace sop
 }  // namespace fde
+
+#if FDE_SOP_TRACE
+// measurement builds only (-DFDE_SOP_TRACE=1): the last k_sop launch's trace
+extern "C" int fde_debug_sop_trace(unsigned long long* host, int n) {
+  if (n > 8192 * 8) n = 8192 * 8;
+  return (int)cudaMemcpyFromSymbol(host, fde::sop::g_sop_trace, sizeof(unsigned long long) * n);
+}
+#endif

@@ -388,31 +388,44 @@ __host__ __device__ constexpr int sop_upc() { return 1; }
 // registers per thread (measured): m = 1024: 144 (7 units = 14 warps per SM);
 // m = 2048: 168 (3 units, 12 warps: no spills, 4% faster than 128 with
 // spills); m = 4096: 128 (2 units; 168 leaves one unit per SM, 10% slower)
+#ifndef FDE_SOP_REG64
+#define FDE_SOP_REG64 144
+#endif
 template <int U>
-__host__ __device__ constexpr int sop_maxreg() { return U <= 32 ? 168 : U == 64 ? 144 : U == 128 ? 168 : 128; }
+__host__ __device__ constexpr int sop_maxreg() { return U <= 32 ? 168 : U == 64 ? FDE_SOP_REG64 : U == 128 ? 168 : 128; }
 
 // One launch = the even part of both directions' operators for every active
 // RHS: CTA b holds units upc·b + s (s < upc); column units first.
+#ifndef FDE_SOP_TRACE
+#define FDE_SOP_TRACE 0   // measurement builds only: per-CTA SM id, global start/end, phase clocks
+#endif
+#if FDE_SOP_TRACE
+__device__ unsigned long long g_sop_trace[8192 * 8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#define SOP_TR(i, v) do { if (threadIdx.x == 0 && blockIdx.x < 8192) g_sop_trace[blockIdx.x * 8 + (i)] = (v); } while (0)
+#else
+#define SOP_TR(i, v) do { } while (0)
+#endif
+
+// One unit (line pair u of RHS rhs) with the RHS's scalars β, ppar (which p̂
+// buffer is p̂_old) and α (the lagged x̂ update); U threads t of slot `slot`,
+// shared buffer sm. Returns the unit's p̂·q̂ partial (every thread).
 template <int U>
-__global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>()) k_sop(SopArgs a) {
+__device__ __forceinline__ double sop_unit(const SopArgs& a, const int rhs, const int u, const int t, const int slot,
+                                           double2* const sm, const double beta, const int ppar,
+                                           const double alpha) {
   using G = Geo<U>;
-  constexpr int M = G::M, UPC = sop_upc<U>();
-  extern __shared__ double2 sop_smem[];
-  const int slot = threadIdx.x / U, t = threadIdx.x - slot * U;
-  double2* const sm = sop_smem + (size_t)slot * G::SLOTS;
-  const int upr = M;                            // units per RHS (2·npairs = m)
-  const int ug = blockIdx.x * UPC + slot;       // unit over the batch
-  const int rhs = ug / upr, u = ug - rhs * upr;
-  SolveState& st = a.st[rhs];
-  if (!st.cyc_active) return;                   // CTA-uniform (upr is a multiple of UPC)
-  const bool col = u < a.npairs;                // CTA-uniform (npairs is a multiple of UPC)
+  constexpr int M = G::M;
+  const bool col = u < a.npairs;                // unit-uniform
   const int g = col ? u : u - a.npairs;
   const int n = a.n, pitch = a.pitch;
   const int l0 = 2 * g, l1 = 2 * g + 1;         // lines of the pair (l1 may be n: padding column / no row)
   const bool v1 = l1 < n;
   const size_t base = (size_t)rhs * n * pitch;
-  const double beta = st.betac;
-  const int ppar = st.ppar;
   const double* __restrict__ pold = ppar ? a.p2 : a.p;
   double* __restrict__ pnew = ppar ? a.p : a.p2;
   const double2 sct = __ldg(a.sc + t);   // sin/cos(πt/m)
@@ -448,7 +461,6 @@ __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>())
     const size_t o0 = base + (size_t)l0 * pitch, o1 = base + (size_t)(v1 ? l1 : l0) * pitch;
     // diagonal ν + ½λ^α_{i+1} + ½λ^β_{j+1} from the μ' tables (½λ_k = 4m² μ'_k)
     const double hy0 = a.lscale * __ldg(a.muy + l0 + 1), hy1 = v1 ? a.lscale * __ldg(a.muy + l1 + 1) : 0.0;
-    const double alpha = st.alpha;
 #pragma unroll
     for (int c = 0; c < 16; c += 4) {
       double z0[4], z1[4], q0[4], q1[4], x0[4], x1[4];
@@ -492,6 +504,9 @@ __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>())
   //      The four transforms are unrolled: each is specialised for its kind
   //      (the runtime-flag version measured slower per transform on the B200).
   double2 xend = make_double2(0.0, 0.0), gend = make_double2(0.0, 0.0);
+#if FDE_SOP_TRACE
+  SOP_TR(3, clock64());
+#endif
 #pragma unroll
   for (int T = 0; T < (FDE_SOP_PROBE == 1 ? 0 : FDE_SOP_PROBE == 2 ? 1 : 4); ++T) {
     transform<U>(v, sm, t, slot, sct, a.tw, xend, gend, T > 0, T == 1 || T == 2);
@@ -513,7 +528,13 @@ __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>())
       if (t == 0) v[0] = make_double2(0.0, 0.0);
       xend = make_double2(0.0, 0.0);
     }
+#if FDE_SOP_TRACE
+    if (T == 1) SOP_TR(4, clock64());
+#endif
   }
+#if FDE_SOP_TRACE
+  SOP_TR(5, clock64());
+#endif
   // ---- store the even part (chunk layout j = 16t + q, element j-1)
   if (col) {
 #pragma unroll
@@ -539,8 +560,34 @@ __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>())
   }
   // ---- p̂·q̂ partial of this unit (slot u); k_sine_xr5 sums them in fixed order
   double* scr = reinterpret_cast<double*>(sm + G::BUF);
-  acc = cta_sum2<U>(acc, scr + 40, t, slot);
+  return cta_sum2<U>(acc, scr + 40, t, slot);
+}
+
+template <int U>
+__global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>()) k_sop(SopArgs a) {
+#if FDE_SOP_TRACE
+  unsigned smid;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+  SOP_TR(0, gtime());
+  SOP_TR(1, smid);
+  SOP_TR(2, clock64());
+#endif
+  using G = Geo<U>;
+  constexpr int UPC = sop_upc<U>();
+  extern __shared__ double2 sop_smem[];
+  const int slot = threadIdx.x / U, t = threadIdx.x - slot * U;
+  double2* const sm = sop_smem + (size_t)slot * G::SLOTS;
+  const int upr = G::M;                         // units per RHS (2·npairs = m)
+  const int ug = blockIdx.x * UPC + slot;       // unit over the batch
+  const int rhs = ug / upr, u = ug - rhs * upr;
+  const SolveState& st = a.st[rhs];
+  if (!st.cyc_active) return;                   // CTA-uniform (upr is a multiple of UPC)
+  const double acc = sop_unit<U>(a, rhs, u, t, slot, sm, st.betac, st.ppar, st.alpha);
   if (t == 0) a.part[(size_t)rhs * KPMAX + u] = acc;
+#if FDE_SOP_TRACE
+  SOP_TR(6, clock64());
+  SOP_TR(7, gtime());
+#endif
 }
 
 }  // namespace sop
