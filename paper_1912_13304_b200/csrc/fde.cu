@@ -298,6 +298,7 @@ struct fde_handle_s {
   double *kx = nullptr, *kb = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kq = nullptr;
   double* kp2 = nullptr;    // second p̂ buffer of the concurrent sine body
   double* kpart = nullptr;  // fused-kernel partials [batch][3][KPMAX]
+  double* gpart = nullptr;  // group sums of the two-level GMRES reductions [batch][64][64]
   double* spart = nullptr;  // r02 operator pass: one p̂·q̂ partial per unit [batch][KPMAX]
   double2* zscr = nullptr;  // variable Toeplitz spectrum scratch [batch][pairs][L]
   double* V = nullptr;
@@ -1031,6 +1032,7 @@ void build(fde_handle h, const fde_desc* d) {
     h->gm_dcgs = !(go && std::strcmp(go, "cgs2") == 0);
   }
   h->part = h->dalloc<double>((size_t)h->batch * (MAX_RESTART + 1) * RED_BLOCKS);
+  h->gpart = h->dalloc<double>((size_t)h->batch * 64 * 64);
   FDE_CUDA(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->st));
   FDE_CUDA(cudaMemsetAsync(h->sst, 0, sizeof(SolveState) * h->batch, h->st));
   FDE_CUDA(cudaStreamSynchronize(h->st));
@@ -1109,6 +1111,7 @@ VecArgs vec_args(fde_handle h, double rtol, int maxit, int restart, int left) {
   a.gs = h->gsm;
   a.ctr = h->ctr;
   a.part = h->part;
+  a.gpart = h->gpart;
   a.rtol = rtol;
   a.maxit = maxit;
   a.restart = restart;
@@ -1124,6 +1127,7 @@ __global__ void k_reset_counters(Counters* c, SolveState* s, int batch) {
     c->loops = 0;
     for (int i = 0; i < 64; ++i) c->tickets[i] = 0u;
   }
+  for (int i = threadIdx.x; i < 8 * 64; i += blockDim.x) c->gtickets[i] = 0u;
   if ((int)threadIdx.x < batch) {
     SolveState& q = s[threadIdx.x];
     q.cyc_active = 1;

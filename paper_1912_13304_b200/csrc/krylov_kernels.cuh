@@ -15,7 +15,20 @@
 #include "pdl.cuh"
 #include "krylov_state.cuh"
 
+
 namespace fde {
+
+#ifndef FDE_SOP_TRACE
+#define FDE_SOP_TRACE 0   // measurement builds only (timeline of the sine body)
+#endif
+#if FDE_SOP_TRACE
+__device__ unsigned long long g_xr_trace[4096];   // [cta][start, α, loop end, end]; [4095] = loop_ctrl
+__device__ __forceinline__ unsigned long long xr_gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#endif
 
 // block-wide sum of NV values; result valid in thread 0. red: smem [NV][32]
 template <int NV>
@@ -93,6 +106,7 @@ struct VecArgs {
   GmresSmall* gs;
   Counters* ctr;
   double* part;          // partial sums [batch][nvec][RED_BLOCKS]
+  double* gpart;         // group sums of the two-level reduction [batch][64 vectors][64 groups]
   double rtol;
   int maxit;
   int restart;
@@ -545,6 +559,56 @@ __global__ void __launch_bounds__(256) k_gm_cgs_ws(VecArgs a, const double* __re
 // with V orthonormal); the cycle ends with one pass A without z for column m-1.
 // Partial slots: a_i at i, b_i at j+i, ν at 2j, c at 2j+1 (2j+2 <= 64: j <= 31).
 
+// Two-level form of last_block + finalize (for passes with many partial
+// vectors): blocks arrive in groups of 16; a group's last block sums its
+// group's partials of every vector (one load per (vector, block), all in
+// flight) into gpart, then the last group sums the ≤ 37 group sums. Fixed
+// order at both levels (deterministic); the serial tail is two short rounds
+// instead of one block summing nvec × gridDim.x partials.
+constexpr int RGS = 16;
+__device__ __forceinline__ bool finalize2(const VecArgs& a, int rb, const double* part, int nvec, double* out) {
+  __shared__ bool s_l;
+  const int G = (int)gridDim.x, grp = blockIdx.x / RGS, ngrp = (G + RGS - 1) / RGS;
+  const int gcnt = min(RGS, G - grp * RGS);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_l = atomicAdd(&a.ctr->gtickets[rb * 64 + grp], 1u) == (unsigned)(gcnt - 1);
+  __syncthreads();
+  if (!s_l) return false;
+  __threadfence();
+  if (threadIdx.x == 0) a.ctr->gtickets[rb * 64 + grp] = 0u;
+  double* gp = a.gpart + (size_t)rb * 64 * 64;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    double v[RGS];
+#pragma unroll
+    for (int b = 0; b < RGS; ++b) v[b] = b < gcnt ? __ldcg(part + (size_t)i * RED_BLOCKS + grp * RGS + b) : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int b = 0; b < RGS; ++b) sum += v[b];
+    gp[i * 64 + grp] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_l = atomicAdd(&a.ctr->tickets[rb * 8], 1u) == (unsigned)(ngrp - 1);
+  __syncthreads();
+  if (!s_l) return false;
+  __threadfence();
+  if (threadIdx.x == 0) a.ctr->tickets[rb * 8] = 0u;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    double v[8];
+    double sum = 0.0;
+    for (int g0 = 0; g0 < ngrp; g0 += 8) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g) v[g] = g0 + g < ngrp ? __ldcg(gp + i * 64 + g0 + g) : 0.0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) sum += v[g];
+    }
+    out[i] = sum;
+  }
+  __syncthreads();
+  return true;
+}
+
 // the finalising block of pass A (all its threads; sums in gs.h[0 .. 2j+1]):
 // thread 0 finalises column j-1 (O(j) serial, on register copies), the
 // block forms the new raw column j in parallel
@@ -567,9 +631,16 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
       ssn[i] = __ldcg(&gs.sn[i]);
     }
   }
-  // (any block size: the passes run with 32..256 threads)
+  // (any block size: the passes run with 32..256 threads); the RHS state the
+  // serial part reads is fetched here too, so thread 0 issues no load of its own
+  __shared__ double s_bnorm, s_cc;
+  __shared__ int s_iters, s_act;
   if (threadIdx.x == (32 % blockDim.x)) s_nu = __ldcg(&gs.h[2 * j]);
   if (threadIdx.x == (64 % blockDim.x) && j >= 1) s_g = __ldcg(&gs.g[j - 1]);
+  if (threadIdx.x == (96 % blockDim.x)) s_bnorm = __ldcg(&s.bnorm);
+  if (threadIdx.x == (128 % blockDim.x)) s_iters = __ldcg(&s.iters);
+  if (threadIdx.x == (160 % blockDim.x)) s_act = __ldcg(&s.cyc_active);
+  if (threadIdx.x == (192 % blockDim.x)) s_cc = has_z ? __ldcg(&gs.h[2 * j + 1]) : 0.0;
   __syncthreads();
   if (threadIdx.x == 0) {
     const double nu = s_nu;
@@ -605,26 +676,27 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
       const double gc = s_g;
       gs.g[c + 1] = -sn * gc;
       gs.g[c] = cn * gc;
-      s.iters += 1;
+      const int its = s_iters + 1;
+      s.iters = its;
       s.kused = j;
-      s.rnorm = fabs(sn * gc) / s.bnorm;
+      s.rnorm = fabs(sn * gc) / s_bnorm;
       if (!isfinite(bet) || !isfinite(den)) {
         s.status = ST_NONFINITE;
         stop = true;
-      } else if (fabs(sn * gc) <= a.rtol * s.bnorm) {
+      } else if (fabs(sn * gc) <= a.rtol * s_bnorm) {
         s.converged = 1;
         stop = true;
       } else if (bet == 0.0) {
         s.status = ST_BREAKDOWN;
         stop = true;
-      } else if (s.iters >= a.maxit || !has_z) {
+      } else if (its >= a.maxit || !has_z) {
         stop = true;  // budget, or the end-of-cycle pass
       }
     } else if (!(bet > 0.0)) {
       s.status = isfinite(bet) ? ST_BREAKDOWN : ST_NONFINITE;
       stop = true;
     }
-    if (stop && s.cyc_active) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
+    if (stop && s_act) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
     s_bet = bet;
     s_stop = stop;
   }
@@ -633,7 +705,7 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
   // pass-B coefficients and the first projection (new raw column j):
   // d = [b, (c - aᵀb)/β], Hr[:, j] = (d - H a)/β with the finalised columns k < j
   const double bi = 1.0 / s_bet;
-  const double cc = has_z ? __ldcg(&gs.h[2 * j + 1]) : 0.0;
+  const double cc = s_cc;
   double ab = 0.0;
   for (int i = 0; i < j; ++i) ab = fma(sa[i], sb[i], ab);
   const double dj = (cc - ab) * bi;
@@ -663,6 +735,10 @@ __global__ void __launch_bounds__(256) k_gm_dcgs_a(VecArgs a, const double* __re
   if (a.ctr->active == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (!a.st[rb].cyc_active) return;
+#if FDE_SOP_TRACE
+  const bool trc = (j == 20 && z != nullptr && rb == 0 && threadIdx.x == 0);
+  if (trc) g_xr_trace[blockIdx.x * 4] = xr_gtime();
+#endif
   const size_t o = (size_t)rb * N;
   const int nv = j;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -724,9 +800,20 @@ __global__ void __launch_bounds__(256) k_gm_dcgs_a(VecArgs a, const double* __re
     part[(size_t)(2 * j) * RED_BLOCKS + blockIdx.x] = nc[0];
     part[(size_t)(2 * j + 1) * RED_BLOCKS + blockIdx.x] = nc[1];
   }
-  if (last_block(&a.ctr->tickets[rb * 8])) {
-    finalize(part, 2 * j + 2, a.gs[rb].h);
+#if FDE_SOP_TRACE
+  if (trc) g_xr_trace[blockIdx.x * 4 + 1] = xr_gtime();
+#endif
+  if (finalize2(a, rb, part, 2 * j + 2, a.gs[rb].h)) {
+#if FDE_SOP_TRACE
+    if (trc) g_xr_trace[4000] = xr_gtime();
+#endif
+#if FDE_SOP_TRACE
+    if (trc) g_xr_trace[4001] = xr_gtime();
+#endif
     dcgs_step(a, rb, j, hz);
+#if FDE_SOP_TRACE
+    if (trc) g_xr_trace[4002] = xr_gtime();
+#endif
   }
 }
 
@@ -753,6 +840,10 @@ __global__ void __launch_bounds__(128) k_gm_dcgs_b2(VecArgs a, const double* __r
   }
   const double dj = __ldcg(&gs.dj), bi = __ldcg(&gs.binv);
   __syncthreads();
+#if FDE_SOP_TRACE
+  const bool trc = (j == 20 && rb == 0 && threadIdx.x == 0);
+  if (trc) g_xr_trace[blockIdx.x * 4 + 2] = xr_gtime();
+#endif
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N; e += gridDim.x * blockDim.x) {
     const double uv = __ldcg(u + o + e), zv = __ldcg(z + o + e);
     double vv[JB];
@@ -768,6 +859,9 @@ __global__ void __launch_bounds__(128) k_gm_dcgs_b2(VecArgs a, const double* __r
     u[o + e] = qv;
     z[o + e] = (zv - sb - dj * qv) * bi;
   }
+#if FDE_SOP_TRACE
+  if (trc) g_xr_trace[blockIdx.x * 4 + 3] = xr_gtime();
+#endif
 }
 
 // end of cycle, step 1: y = R⁻¹ g (redundantly per block), u = Σ y_i V_i
@@ -1046,17 +1140,6 @@ __global__ void k_pcg_xrz_none(KryFuse k, int N, double* __restrict__ z) {
   kry_reduce_finalize(k, acc);
 }
 
-#ifndef FDE_SOP_TRACE
-#define FDE_SOP_TRACE 0   // measurement builds only (timeline of the sine body)
-#endif
-#if FDE_SOP_TRACE
-__device__ unsigned long long g_xr_trace[4096];   // [cta][start, end]; [2048] = loop_ctrl
-__device__ __forceinline__ unsigned long long xr_gtime() {
-  unsigned long long v;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
-  return v;
-}
-#endif
 
 // while-loop control of a CUDA graph (conditional WHILE node): keep looping
 // while some RHS is still iterating, at most maxloops bodies.
@@ -1065,7 +1148,7 @@ __global__ void k_loop_ctrl(cudaGraphConditionalHandle hdl, Counters* c, int max
   const int loops = c->loops + 1;
   c->loops = loops;
 #if FDE_SOP_TRACE
-  g_xr_trace[2048] = xr_gtime();
+  g_xr_trace[4095] = xr_gtime();
 #endif
   cudaGraphSetConditional(hdl, (c->active > 0 && loops < maxloops) ? 1u : 0u);
 }

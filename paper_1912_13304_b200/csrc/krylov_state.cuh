@@ -55,6 +55,7 @@ struct Counters {            // device counters
   int loops;                 // while-loop bodies executed (launch accounting)
   int pad;
   unsigned tickets[64];      // per-RHS last-block tickets (batch <= 8, 8 slots each)
+  unsigned gtickets[8 * 64]; // per-RHS group tickets of the two-level reductions (64 groups of 16 blocks)
 };
 
 // 1/x to ~1 ulp for 1e-30 < x < 1e30: fp32 seed + two Newton steps (FP64 FMA),

@@ -495,13 +495,33 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
   FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
 #if FDE_SOP_TRACE
-  if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 2] = xr_gtime();
+  if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 4] = xr_gtime();
 #endif
   if (!k.st[rhs].cyc_active) return;
   __shared__ double s_pq[8];
+  const int pitch = 1 << lgp;
+  const size_t o = (size_t)rhs * ((size_t)n << lgp);
+  const int nq = (n << lgp) >> 2;
+  double* __restrict__ rr = k.r + o;
+  double* __restrict__ zz = k.q + o;
+  const double* __restrict__ wr = wr_ + o;
+  const double* __restrict__ wc = wc_ + o;
+  const double* __restrict__ pp = (k.st[rhs].ppar ? k.p : k.p2) + o;
+  const int T = gridDim.x * blockDim.x;
+  const int c0 = blockIdx.x * blockDim.x + threadIdx.x;
+  // the first group's vectors are in flight while the unit partials are summed
+  dbl4 rv, av, bv, pv;
+  {
+    const size_t e = (size_t)(c0 < nq ? c0 : 0) * 4;
+    rv = ld4(rr + e);
+    av = ld4(wr + e);
+    bv = ld4(wc + e);
+    pv = ld4(pp + e);
+  }
   {
     const double* sp = spart + (size_t)rhs * KPMAX;
     double v = 0.0;
+#pragma unroll 4
     for (int i = threadIdx.x; i < nsp; i += blockDim.x) v += __ldcg(sp + i);
     v = warp_sum(v);
     if ((threadIdx.x & 31) == 0) s_pq[threadIdx.x >> 5] = v;
@@ -512,21 +532,19 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
   for (int w = 0; w < 8; ++w) pq += s_pq[w];
   const bool spd = pq > 0.0;
   const double al = spd ? k.st[rhs].rho / pq : 0.0;
-  const int pitch = 1 << lgp;
-  const size_t o = (size_t)rhs * ((size_t)n << lgp);
-  const int nq = (n << lgp) >> 2;
-  double* __restrict__ rr = k.r + o;
-  double* __restrict__ zz = k.q + o;
-  const double* __restrict__ wr = wr_ + o;
-  const double* __restrict__ wc = wc_ + o;
-  const double* __restrict__ pp = (k.st[rhs].ppar ? k.p : k.p2) + o;
-  const int T = gridDim.x * blockDim.x;
+#if FDE_SOP_TRACE
+  if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 4 + 1] = xr_gtime();
+#endif
   double acc[3] = {0.0, 0.0, 0.0};
   if (spd) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nq; c += T) {
+    for (int c = c0; c < nq; c += T) {
       const size_t e = (size_t)c * 4;
-      dbl4 rv = ld4(rr + e);
-      const dbl4 av = ld4(wr + e), bv = ld4(wc + e), pv = ld4(pp + e);
+      if (c != c0) {
+        rv = ld4(rr + e);
+        av = ld4(wr + e);
+        bv = ld4(wc + e);
+        pv = ld4(pp + e);
+      }
       const int j = (int)(e >> lgp), i = (int)e & (pitch - 1);
       const double fy = Fy[j], dy = hy[j];
       dbl4 zv;
@@ -550,12 +568,15 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
       st4(zz + e, zv);
     }
   }
+#if FDE_SOP_TRACE
+  if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 4 + 2] = xr_gtime();
+#endif
   KryFuse kk = k;
   kk.mode = k.mode | KM_SOPA;
   kk.xval = pq;   // every CTA summed the same partials in the same order: the finaliser's α is this CTA's α
   kry_reduce_finalize(kk, acc);
 #if FDE_SOP_TRACE
-  if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 2 + 1] = xr_gtime();
+  if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 4 + 3] = xr_gtime();
 #endif
 }
 

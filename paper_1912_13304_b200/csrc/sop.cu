@@ -8,15 +8,27 @@
 namespace fde {
 namespace sop {
 
-template <int U>
-static cudaError_t launch_u(const SopArgs& a, cudaStream_t st) {
+template <int U, bool ONEWAVE>
+static cudaError_t launch_k(const SopArgs& a, cudaStream_t st) {
   constexpr int UPC = sop_upc<U>();
   const size_t smem = (size_t)UPC * Geo<U>::SLOTS * sizeof(double2);
-  auto kern = k_sop<U>;
+  auto kern = k_sop<U, ONEWAVE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<a.total_warps / UPC, U * UPC, smem, st>>>(a);   // total_warps: units over the batch
   return cudaGetLastError();
+}
+
+// m = 1024: the 128-register instantiation when every unit of the launch is
+// resident at once (8 per SM), else 144 (sop_maxreg)
+template <int U>
+static cudaError_t launch_u(const SopArgs& a, cudaStream_t st) {
+  if (U != 64) return launch_k<U, false>(a, st);
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  return a.total_warps <= 8 * sms ? launch_k<U, true>(a, st) : launch_k<U, false>(a, st);
 }
 
 bool supported(int m) { return m == 512 || m == 1024 || m == 2048 || m == 4096; }

@@ -385,14 +385,18 @@ __device__ __forceinline__ void transform(double2 (&v)[16], double2* sm, int t, 
 // one full 32-byte sector per row, through L1) was slower than one
 template <int U>
 __host__ __device__ constexpr int sop_upc() { return 1; }
-// registers per thread (measured): m = 1024: 144 (7 units = 14 warps per SM);
-// m = 2048: 168 (3 units, 12 warps: no spills, 4% faster than 128 with
-// spills); m = 4096: 128 (2 units; 168 leaves one unit per SM, 10% slower)
-#ifndef FDE_SOP_REG64
-#define FDE_SOP_REG64 144
-#endif
-template <int U>
-__host__ __device__ constexpr int sop_maxreg() { return U <= 32 ? 168 : U == 64 ? FDE_SOP_REG64 : U == 128 ? 168 : 128; }
+// registers per thread (measured). An SMSP holds 16 K registers, so a warp
+// at R registers fits ⌊16384/(32R)⌋ times per SMSP: 144 → 3 warps per SMSP,
+// 6 two-warp units per SM; 128 → 4, 8 units. m = 1024: 144 (56 B of spills)
+// when the units exceed one wave at 128 (batch ≥ 2), 128 (336 B of spills)
+// when all units of the launch fit one wave of 8 per SM (batch 1: 1024 ≤
+// 8·148; the 136 second-wave units of the 144-register kernel end the launch
+// 2.5 µs later); m = 2048: 168 (3 units, 12 warps: no spills, 4% faster than
+// 128 with spills); m = 4096: 128 (2 units; 168 leaves one, 10% slower)
+template <int U, bool ONEWAVE>
+__host__ __device__ constexpr int sop_maxreg() {
+  return U <= 32 ? 168 : U == 64 ? (ONEWAVE ? 128 : 144) : U == 128 ? 168 : 128;
+}
 
 // One launch = the even part of both directions' operators for every active
 // RHS: CTA b holds units upc·b + s (s < upc); column units first.
@@ -563,8 +567,8 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const int rhs, cons
   return cta_sum2<U>(acc, scr + 40, t, slot);
 }
 
-template <int U>
-__global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__(sop_maxreg<U>()) k_sop(SopArgs a) {
+template <int U, bool ONEWAVE>
+__global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__((sop_maxreg<U, ONEWAVE>())) k_sop(SopArgs a) {
 #if FDE_SOP_TRACE
   unsigned smid;
   asm volatile("mov.u32 %0, %smid;" : "=r"(smid));

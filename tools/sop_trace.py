@@ -59,12 +59,12 @@ out["first_blocks_sm"] = [int(s) for s in sm[:24]]
 xb = (ctypes.c_ulonglong * 4096)()
 if fde.lib.fde_debug_xr_trace(xb, 4096) == 0:
     xa = np.frombuffer(xb, dtype=np.uint64).astype(np.int64)
-    xs, xe = xa[0:1184:2], xa[1:1184:2]
-    ok = xs > 0
-    out["timeline_us"] = {"sop_first_start": 0.0, "sop_last_end": float((g7.max() - t0) / 1e3),
-                          "xr_first_start": float((xs[ok].min() - t0) / 1e3),
-                          "xr_last_start": float((xs[ok].max() - t0) / 1e3),
-                          "xr_last_end": float((xe[ok].max() - t0) / 1e3),
-                          "ctrl": float((xa[2048] - t0) / 1e3)}
+    xt = xa[:4092].reshape(1023, 4)
+    xt = xt[xt[:, 0] > 0]
+    rel = lambda v: [round(float((v.min() - t0) / 1e3), 2), round(float((v.mean() - t0) / 1e3), 2),
+                     round(float((v.max() - t0) / 1e3), 2)]
+    out["timeline_us"] = {"sop_last_end": float((g7.max() - t0) / 1e3), "xr_ctas": int(len(xt)),
+                          "xr_start": rel(xt[:, 0]), "xr_alpha": rel(xt[:, 1]), "xr_loop_end": rel(xt[:, 2]),
+                          "xr_end": rel(xt[:, 3]), "ctrl": float((xa[4095] - t0) / 1e3)}
 print(json.dumps(out))
 h.close()
