@@ -494,10 +494,13 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
                                                      int nsp) {
   FDE_PDL_ENTRY();
   const int rhs = blockIdx.y;
+  const SolveState& st0 = k.st[rhs];   // the RHS state in one round trip
+  const int act = st0.cyc_active, ppar = st0.ppar;
+  const double rho = st0.rho;
+  if (!act) return;
 #if FDE_SOP_TRACE
   if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 4] = xr_gtime();
 #endif
-  if (!k.st[rhs].cyc_active) return;
   __shared__ double s_pq[8];
   const int pitch = 1 << lgp;
   const size_t o = (size_t)rhs * ((size_t)n << lgp);
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
   double* __restrict__ zz = k.q + o;
   const double* __restrict__ wr = wr_ + o;
   const double* __restrict__ wc = wc_ + o;
-  const double* __restrict__ pp = (k.st[rhs].ppar ? k.p : k.p2) + o;
+  const double* __restrict__ pp = (ppar ? k.p : k.p2) + o;
   const int T = gridDim.x * blockDim.x;
   const int c0 = blockIdx.x * blockDim.x + threadIdx.x;
   // the first group's vectors are in flight while the unit partials are summed
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
 #pragma unroll
   for (int w = 0; w < 8; ++w) pq += s_pq[w];
   const bool spd = pq > 0.0;
-  const double al = spd ? k.st[rhs].rho / pq : 0.0;
+  const double al = spd ? rho / pq : 0.0;
 #if FDE_SOP_TRACE
   if (threadIdx.x == 0 && blockIdx.y == 0) g_xr_trace[blockIdx.x * 4 + 1] = xr_gtime();
 #endif

@@ -569,13 +569,6 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const int rhs, cons
 
 template <int U, bool ONEWAVE>
 __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__((sop_maxreg<U, ONEWAVE>())) k_sop(SopArgs a) {
-#if FDE_SOP_TRACE
-  unsigned smid;
-  asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-  SOP_TR(0, gtime());
-  SOP_TR(1, smid);
-  SOP_TR(2, clock64());
-#endif
   using G = Geo<U>;
   constexpr int UPC = sop_upc<U>();
   extern __shared__ double2 sop_smem[];
@@ -586,6 +579,13 @@ __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__((sop_maxreg<U, O
   const int rhs = ug / upr, u = ug - rhs * upr;
   const SolveState& st = a.st[rhs];
   if (!st.cyc_active) return;                   // CTA-uniform (upr is a multiple of UPC)
+#if FDE_SOP_TRACE
+  unsigned smid;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+  SOP_TR(0, gtime());
+  SOP_TR(1, smid);
+  SOP_TR(2, clock64());
+#endif
   const double acc = sop_unit<U>(a, rhs, u, t, slot, sm, st.betac, st.ppar, st.alpha);
   if (t == 0) a.part[(size_t)rhs * KPMAX + u] = acc;
 #if FDE_SOP_TRACE
