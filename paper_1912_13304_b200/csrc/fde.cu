@@ -1501,6 +1501,9 @@ fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int ma
 }
 
 // ---------------------------------------------------------------- GMRES
+#ifndef FDE_GMA_EPL4
+#define FDE_GMA_EPL4 4   // elements per lane of DCGS2 pass A for j >= 16 (4 basis vectors per warp)
+#endif
 void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
   const int* gA = &h->ctr->active;
   const int* gU = &h->ctr->unfinished;
@@ -1517,7 +1520,7 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
     auto pick = [&](int j, auto&& f) {
       if (j < 8) f(std::integral_constant<int, 1>{}, std::integral_constant<int, 16>{}, std::integral_constant<int, 8>{});
       else if (j < 16) f(std::integral_constant<int, 2>{}, std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{});
-      else f(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}, std::integral_constant<int, 32>{});
+      else f(std::integral_constant<int, 4>{}, std::integral_constant<int, FDE_GMA_EPL4>{}, std::integral_constant<int, 32>{});
     };
     for (int j = 0; j <= restart; ++j) {
       double* Vj = V + (size_t)j * vs;
@@ -1544,7 +1547,14 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
           launch_k(h->st, k_gm_dcgs_a<ns, epl>, ggrid(32 * epl), RED_THREADS, 0, va, V, vs, (const double*)Vj,
                    (const double*)Vn, j);
         });
-        launch_named(h, "gm_dcgs_b", [&] { launch_k(h->st, k_gm_dcgs_b2<jb>, sgrid, 128, 0, va, V, vs, Vj, Vn, j); });
+        // pass B with 8 slots for j < 6, else 32: ptxas schedules the 16-slot
+        // instantiation with its loads interleaved into the FMA chain (36
+        // registers, round trips serialised: j = 15 took 65.5 µs against
+        // 35.3 with 32 slots), while at small j the 32-slot one is latency-
+        // bound (j = 0: 20.6 vs 11.6 µs)
+        (void)jb;
+        if (j < 6) launch_named(h, "gm_dcgs_b", [&] { launch_k(h->st, k_gm_dcgs_b2<8>, sgrid, 128, 0, va, V, vs, Vj, Vn, j); });
+        else launch_named(h, "gm_dcgs_b", [&] { launch_k(h->st, k_gm_dcgs_b2<32>, sgrid, 128, 0, va, V, vs, Vj, Vn, j); });
       });
     }
   } else
@@ -1976,5 +1986,11 @@ fde_status fde_profile_unit(fde_handle h, const double* x, double* y, double* z,
 extern "C" int fde_debug_xr_trace(unsigned long long* host, int n) {
   if (n > 4096) n = 4096;
   return (int)cudaMemcpyFromSymbol(host, fde::g_xr_trace, sizeof(unsigned long long) * n);
+}
+// reset: per-step min slots (2048 + 4j) to ~0, everything else to 0
+extern "C" int fde_debug_xr_trace_reset() {
+  std::vector<unsigned long long> v(4096, 0ull);
+  for (int j = 0; j < 64; ++j) v[3000 + 4 * j] = ~0ull;
+  return (int)cudaMemcpyToSymbol(fde::g_xr_trace, v.data(), sizeof(unsigned long long) * 4096);
 }
 #endif

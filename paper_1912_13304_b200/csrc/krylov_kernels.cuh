@@ -642,6 +642,9 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
   if (threadIdx.x == (160 % blockDim.x)) s_act = __ldcg(&s.cyc_active);
   if (threadIdx.x == (192 % blockDim.x)) s_cc = has_z ? __ldcg(&gs.h[2 * j + 1]) : 0.0;
   __syncthreads();
+#if FDE_SOP_TRACE
+  if (j == 20 && has_z && rb == 0 && threadIdx.x == 0) g_xr_trace[4003] = xr_gtime();
+#endif
   if (threadIdx.x == 0) {
     const double nu = s_nu;
     double aa = 0.0;
@@ -701,6 +704,9 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
     s_stop = stop;
   }
   __syncthreads();
+#if FDE_SOP_TRACE
+  if (j == 20 && has_z && rb == 0 && threadIdx.x == 0) g_xr_trace[4004] = xr_gtime();
+#endif
   if (s_stop) return;
   // pass-B coefficients and the first projection (new raw column j):
   // d = [b, (c - aᵀb)/β], Hr[:, j] = (d - H a)/β with the finalised columns k < j
@@ -728,7 +734,7 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
 
 // pass A (z == nullptr: the end-of-cycle pass, a and ν only)
 template <int NS, int EPL>
-__global__ void __launch_bounds__(256) k_gm_dcgs_a(VecArgs a, const double* __restrict__ V, size_t vstride,
+__global__ void __launch_bounds__(256, NS * EPL > 16 ? 2 : 4) k_gm_dcgs_a(VecArgs a, const double* __restrict__ V, size_t vstride,
                                                    const double* __restrict__ u, const double* __restrict__ z, int j) {
   FDE_PDL_ENTRY();
   constexpr int CH = 32 * EPL;
@@ -738,6 +744,7 @@ __global__ void __launch_bounds__(256) k_gm_dcgs_a(VecArgs a, const double* __re
 #if FDE_SOP_TRACE
   const bool trc = (j == 20 && z != nullptr && rb == 0 && threadIdx.x == 0);
   if (trc) g_xr_trace[blockIdx.x * 4] = xr_gtime();
+  if (z != nullptr && rb == 0 && threadIdx.x == 0) atomicMin(&g_xr_trace[3000 + j * 4], xr_gtime());
 #endif
   const size_t o = (size_t)rb * N;
   const int nv = j;
@@ -802,6 +809,7 @@ __global__ void __launch_bounds__(256) k_gm_dcgs_a(VecArgs a, const double* __re
   }
 #if FDE_SOP_TRACE
   if (trc) g_xr_trace[blockIdx.x * 4 + 1] = xr_gtime();
+  if (z != nullptr && rb == 0 && threadIdx.x == 0) atomicMax(&g_xr_trace[3000 + j * 4 + 1], xr_gtime());
 #endif
   if (finalize2(a, rb, part, 2 * j + 2, a.gs[rb].h)) {
 #if FDE_SOP_TRACE
@@ -813,6 +821,7 @@ __global__ void __launch_bounds__(256) k_gm_dcgs_a(VecArgs a, const double* __re
     dcgs_step(a, rb, j, hz);
 #if FDE_SOP_TRACE
     if (trc) g_xr_trace[4002] = xr_gtime();
+    if (hz && rb == 0 && threadIdx.x == 0) g_xr_trace[3000 + j * 4 + 2] = xr_gtime();
 #endif
   }
 }
@@ -861,6 +870,7 @@ __global__ void __launch_bounds__(128) k_gm_dcgs_b2(VecArgs a, const double* __r
   }
 #if FDE_SOP_TRACE
   if (trc) g_xr_trace[blockIdx.x * 4 + 3] = xr_gtime();
+  if (rb == 0 && threadIdx.x == 0) atomicMax(&g_xr_trace[3000 + j * 4 + 3], xr_gtime());
 #endif
 }
 
