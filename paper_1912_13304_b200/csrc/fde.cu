@@ -279,7 +279,8 @@ struct fde_handle_s {
   // r02 sine-domain operator (sop.cu): DCT-split tables
   bool sop_ok = false;
   double *sop_hx = nullptr, *sop_hy = nullptr, *sop_mux = nullptr, *sop_muy = nullptr;
-  double2 *sop_tw = nullptr, *sop_sc = nullptr;
+  double2 *sop_tw = nullptr, *sop_sc = nullptr, *sop_twA = nullptr;
+  double *sop_muxL = nullptr, *sop_muyL = nullptr;
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
   double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
   double *invF = nullptr, *Fx = nullptr, *Fy = nullptr;
@@ -922,6 +923,22 @@ void build(fde_handle h, const fde_desc* d) {
     }
     h->sop_tw = h->upload(tw);
     h->sop_sc = h->upload(sc);
+    // lane-major copies for the kernel's strided-by-thread reads (U = m/16 threads)
+    const int U = m / 16;
+    std::vector<double2> twA(4 * U);
+    for (int i = 0; i < 4; ++i)
+      for (int t = 0; t < U; ++t) twA[i * U + t] = tw[(size_t)t << i];
+    std::vector<double> muxL(m + 1), muyL(m + 1);
+    for (int t = 0; t < U; ++t)
+      for (int q = 0; q < 16; ++q) {
+        muxL[q * U + t] = mux[16 * t + q];
+        muyL[q * U + t] = muy[16 * t + q];
+      }
+    muxL[m] = mux[m];
+    muyL[m] = muy[m];
+    h->sop_twA = h->upload(twA);
+    h->sop_muxL = h->upload(muxL);
+    h->sop_muyL = h->upload(muyL);
   }
 
   // preconditioner tables
@@ -1331,6 +1348,9 @@ fde::sop::SopArgs sop_args(fde_handle h) {
   sa.mux = h->sop_mux;
   sa.muy = h->sop_muy;
   sa.tw = h->sop_tw;
+  sa.twA = h->sop_twA;
+  sa.muxL = h->sop_muxL;
+  sa.muyL = h->sop_muyL;
   sa.sc = h->sop_sc;
   sa.st = h->sst;
   sa.ctr = h->ctr;

@@ -28,7 +28,10 @@ static cudaError_t launch_u(const SopArgs& a, cudaStream_t st) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  return a.total_warps <= 8 * sms ? launch_k<U, true>(a, st) : launch_k<U, false>(a, st);
+#ifndef FDE_SOP_ONEWAVE
+#define FDE_SOP_ONEWAVE 1
+#endif
+  return (FDE_SOP_ONEWAVE && a.total_warps <= 8 * sms) ? launch_k<U, true>(a, st) : launch_k<U, false>(a, st);
 }
 
 bool supported(int m) { return m == 512 || m == 1024 || m == 2048 || m == 4096; }

@@ -54,6 +54,9 @@ struct SopArgs {
   const double* mux;          // μ'_k = λ^α_k/(8m²), k = 0..m (row direction)
   const double* muy;          // μ'_k = λ^β_k/(8m²) (column direction)
   const double2* tw;          // ω_m^e = exp(-2πi e/m), e < m/2
+  const double2* twA;         // lane-major first-pass base powers: twA[i·U + t] = ω_m^{t·2^i}, i < 4
+  const double* muxL;         // lane-major μ' (row direction): muxL[q·U + t] = μ'_{16t+q}, muxL[m] = μ'_m
+  const double* muyL;         // the same for the column direction
   const double2* sc;          // (sin(πt/m), cos(πt/m)), t < U = m/16
   SolveState* st;
   Counters* ctr;
@@ -197,6 +200,31 @@ __device__ __forceinline__ void twiddle16(double2 (&v)[16], const double2* __res
 }
 
 
+// The same with the four base powers from a lane-major table: b[i] =
+// twA[i·U + t] = ω_m^{t·2^i} (a warp's load is 32 consecutive entries, 4 L1
+// wavefronts, against up to 32 for the lane-strided ω_m^{t·2^i} of the table)
+template <int U>
+__device__ __forceinline__ void twiddle16_lm(double2 (&v)[16], const double2* __restrict__ twA, int t) {
+  double2 b[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned idx = (unsigned)(i * U + t);
+    asm volatile("{\n\t.reg .u64 a;\n\tmul.wide.u32 a, %2, 16;\n\tadd.u64 a, a, %3;\n\t"
+                 "ld.global.nc.v2.f64 {%0, %1}, [a];\n\t}"
+                 : "=d"(b[i].x), "=d"(b[i].y) : "r"(idx), "l"(twA));
+  }
+  const double2 l1 = b[0], l2 = b[1], l3 = cmul(b[0], b[1]);
+  const double2 h4 = b[2], h8 = b[3], h12 = cmul(b[2], b[3]);
+#pragma unroll
+  for (int r = 1; r < 16; ++r) {
+    const int e = brev(r, 4), lo = e & 3, hi = e & 12;
+    const double2 wl = lo == 1 ? l1 : (lo == 2 ? l2 : l3);
+    const double2 wh = hi == 4 ? h4 : (hi == 8 ? h8 : h12);
+    const double2 w = lo == 0 ? wh : (hi == 0 ? wl : cmul(wh, wl));
+    v[r] = cmul(v[r], w);
+  }
+}
+
 // One real transform of size m for the packed pair in v (16 points / thread).
 //   in_chunk: v holds x_j at j = 16t + q (else the stride layout j = t + U·q)
 //   cos = false: G_j = 2 Σ_{i=1}^{m-1} x_i sin(πij/m)      (x_0, x_m ignored)
@@ -205,7 +233,8 @@ __device__ __forceinline__ void twiddle16(double2 (&v)[16], const double2* __res
 // Output: v[q] = G_j at j = 16t + q (chunk layout), j = 0..m-1.
 template <int U>
 __device__ __forceinline__ void transform(double2 (&v)[16], double2* sm, int t, int slot, double2 sct,
-                                          const double2* __restrict__ tw, double2 xend, double2& gend,
+                                          const double2* __restrict__ tw, const double2* __restrict__ twA,
+                                          double2 xend, double2& gend,
                                           const bool in_chunk, const bool cos_) {
   using G = Geo<U>;
   constexpr int M = G::M, B = G::B, LB = G::LB;
@@ -266,7 +295,7 @@ __device__ __forceinline__ void transform(double2 (&v)[16], double2* sm, int t, 
   }
   // 2. radix-16 DIF over q: register q holds k0 = brev4(q); twiddle ω_m^{t·k0}
   dif_reg<4, 0, 16>(v);
-  twiddle16(v, tw, t, 1);            // ω_m^{t·2^i}: t·8 < m/2
+  twiddle16_lm<U>(v, twA, t);        // ω_m^{t·2^i}: t·8 < m/2 (lane-major copy)
   // 3. exchange: (t, k0) -> thread t' = k0 + 16·tl takes th = 0..15
   ubar<U>(slot);
 #pragma unroll
@@ -513,14 +542,14 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const int rhs, cons
 #endif
 #pragma unroll
   for (int T = 0; T < (FDE_SOP_PROBE == 1 ? 0 : FDE_SOP_PROBE == 2 ? 1 : 4); ++T) {
-    transform<U>(v, sm, t, slot, sct, a.tw, xend, gend, T > 0, T == 1 || T == 2);
+    transform<U>(v, sm, t, slot, sct, a.tw, a.twA, xend, gend, T > 0, T == 1 || T == 2);
     if (T == 1) {
       // μ' ⊙ c' and the spectral share of p̂·q̂: Σ_k w_k μ'_k c'_k²
-      const double* __restrict__ mu = col ? a.muy : a.mux;
+      const double* __restrict__ mu = col ? a.muyL : a.muxL;   // lane-major: entry q·U + t = μ'_{16t+q}
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int kk = 16 * t + q;
-        const double mk = __ldg(mu + kk);
+        const double mk = __ldg(mu + q * U + t);
         const double wk = (kk == 0) ? 0.5 : 1.0;
         acc = fma(wk * mk, fma(v[q].x, v[q].x, v[q].y * v[q].y), acc);
         v[q] = make_double2(mk * v[q].x, mk * v[q].y);
