@@ -281,6 +281,9 @@ struct fde_handle_s {
   double *sop_hx = nullptr, *sop_hy = nullptr, *sop_mux = nullptr, *sop_muy = nullptr;
   double2 *sop_tw = nullptr, *sop_sc = nullptr, *sop_twA = nullptr;
   double *sop_muxL = nullptr, *sop_muyL = nullptr;
+  fde::sop::SopMaps sop_maps;                // TMA descriptors of ẑ, p̂, p̂₂ (column staging)
+  bool sop_maps_ok = false;
+  const double *sop_maps_z = nullptr, *sop_maps_p = nullptr;
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
   double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
   double *invF = nullptr, *Fx = nullptr, *Fy = nullptr;
@@ -1378,7 +1381,13 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
   if ((1 << lgp) != h->sine_pitch || lgp < 2) throw FdeFail{FDE_ERR_UNSUPPORTED, "sine pitch is not a power of two"};
   if (h->sop_ok) {
     const fde::sop::SopArgs sa = sop_args(h);
-    launch_named(h, "sine_op_sop", [&] { FDE_CUDA(fde::sop::launch(sa, h->st)); });
+    if (!h->sop_maps_ok || h->sop_maps_z != h->kq || h->sop_maps_p != h->kp) {
+      FDE_CUDA(fde::sop::make_maps(&h->sop_maps, h->kq, h->kp, h->kp2, h->n, h->sine_pitch, h->batch));
+      h->sop_maps_ok = true;
+      h->sop_maps_z = h->kq;
+      h->sop_maps_p = h->kp;
+    }
+    launch_named(h, "sine_op_sop", [&] { FDE_CUDA(fde::sop::launch(sa, h->sop_maps, h->st)); });
     KryFuse kv = kf;
     kv.mode = KM_XR | KM_RZ | KM_GATE;
     const double *Fx = h->Fx, *Fy = h->Fy, *wr = h->wx, *wc = h->wy, *hx = h->sop_hx, *hy = h->sop_hy;

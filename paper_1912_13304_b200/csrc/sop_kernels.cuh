@@ -31,6 +31,7 @@
 // spectral share of p̂·q̂ is Σ_k w_k μ'_k c'_k² (c' = the T2 output, w = ½ at
 // k = 0, m): p̂·D_s C1 μ C D_s p̂ = (D_s p̂)·C1 μ C (D_s p̂) = Σ_k w_k μ_k c_k².
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -62,6 +63,51 @@ struct SopArgs {
   Counters* ctr;
   double* part;               // [batch][KPMAX]: this kernel's per-unit p̂·q̂ partials (k_sine_xr5 sums them)
 };
+
+// ---------------------------------------------------------------- TMA
+// Column units stage their two columns of ẑ / p̂_old (16 B per row, one row
+// per element) with 2D-tile TMA loads (box 2 × 256 rows of the 3D tensor
+// [batch][n][pitch]) into the unit's shared buffer, instead of one scattered
+// 16-byte load per row per thread (a warp's LDG.128 then touched 32 cache
+// lines: 32 L1 tag wavefronts per instruction).
+#ifndef FDE_SOP_TMA
+#define FDE_SOP_TMA 2   // 0: scattered loads; 1: ẑ by TMA, p̂_old scattered; 2: both by TMA (sequential)
+#endif
+struct alignas(64) SopMaps {
+  CUtensorMap z, p, p2;      // ẑ, p̂ buffer 0, p̂ buffer 1
+};
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "SOP_MBW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SOP_MBW_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// one column pair (columns c, c+1, rows 0..M-1 of RHS rhs; row n is outside
+// the tensor and arrives as zeros) into dst (dense: row r at dst[r])
+template <int M>
+__device__ __forceinline__ void tma_columns(double2* dst, const CUtensorMap* map, int c, int rhs, uint64_t* bar) {
+  mbar_expect_tx(bar, M * 16);
+#pragma unroll
+  for (int b = 0; b < M / 256; ++b) tma_load_3d(dst + 256 * b, map, c, 256 * b, rhs, bar);
+}
 
 // ---------------------------------------------------------------- complex
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -448,9 +494,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 // buffer is p̂_old) and α (the lagged x̂ update); U threads t of slot `slot`,
 // shared buffer sm. Returns the unit's p̂·q̂ partial (every thread).
 template <int U>
-__device__ __forceinline__ double sop_unit(const SopArgs& a, const int rhs, const int u, const int t, const int slot,
-                                           double2* const sm, const double beta, const int ppar,
-                                           const double alpha) {
+__device__ __forceinline__ double sop_unit(const SopArgs& a, const SopMaps* maps, const int rhs, const int u,
+                                           const int t, const int slot, double2* const sm, const double beta,
+                                           const int ppar, const double alpha) {
   using G = Geo<U>;
   constexpr int M = G::M;
   const bool col = u < a.npairs;                // unit-uniform
@@ -472,6 +518,45 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const int rhs, cons
   if (FDE_SOP_PROBE == 3) {
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = make_double2(1e-3 * (t + q), 2e-3 * q);
+  } else if (col && FDE_SOP_TMA) {
+    // ẑ (and p̂_old) columns by TMA into the unit's buffer, read back in the
+    // stride layout (row j-1 at buf[j-1]: consecutive lanes, conflict-free)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(sm + G::BUF) + 56);
+    if (t == 0) {
+      mbar_init(bar);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma_columns<M>(sm, &maps->z, l0, rhs, bar);
+    }
+    if (FDE_SOP_TMA == 1) {   // p̂_old scattered, in flight with the ẑ tile
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int j = t + U * q;
+        v[q] = __ldcg(reinterpret_cast<const double2*>(pold + base + (size_t)(j >= 1 ? j - 1 : 0) * pitch + l0));
+      }
+    }
+    ubar<U>(slot);   // the barrier is initialised before anyone waits on it
+    mbar_wait(bar, 0);
+    if (FDE_SOP_TMA == 2) {   // v = ẑ, then p̂_old by a second tile into the same buffer
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int j = t + U * q;
+        v[q] = sm[j >= 1 ? j - 1 : 0];
+      }
+      ubar<U>(slot);   // every thread has read ẑ before the buffer is refilled
+      if (t == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_columns<M>(sm, ppar ? &maps->p2 : &maps->p, l0, rhs, bar);
+      }
+      mbar_wait(bar, 1);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {   // p̂ = ẑ + β p̂_old (the buffer holds p̂_old (2) or ẑ (1))
+      const int j = t + U * q;
+      const double2 w = sm[j >= 1 ? j - 1 : 0];
+      const double2 zq = FDE_SOP_TMA == 2 ? v[q] : w, pq = FDE_SOP_TMA == 2 ? w : v[q];
+      const double p0 = fma(beta, pq.x, zq.x), p1 = fma(beta, pq.y, zq.y);
+      v[q] = j >= 1 ? make_double2(p0, v1 ? p1 : 0.0) : make_double2(0.0, 0.0);
+    }
   } else if (col) {
 #pragma unroll
     for (int c = 0; c < 16; c += 8) {   // 8 points per thread in flight per array
@@ -597,7 +682,8 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const int rhs, cons
 }
 
 template <int U, bool ONEWAVE>
-__global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__((sop_maxreg<U, ONEWAVE>())) k_sop(SopArgs a) {
+__global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__((sop_maxreg<U, ONEWAVE>()))
+    k_sop(SopArgs a, const __grid_constant__ SopMaps maps) {
   using G = Geo<U>;
   constexpr int UPC = sop_upc<U>();
   extern __shared__ double2 sop_smem[];
@@ -615,7 +701,7 @@ __global__ void __launch_bounds__(U * sop_upc<U>()) __maxnreg__((sop_maxreg<U, O
   SOP_TR(1, smid);
   SOP_TR(2, clock64());
 #endif
-  const double acc = sop_unit<U>(a, rhs, u, t, slot, sm, st.betac, st.ppar, st.alpha);
+  const double acc = sop_unit<U>(a, &maps, rhs, u, t, slot, sm, st.betac, st.ppar, st.alpha);
   if (t == 0) a.part[(size_t)rhs * KPMAX + u] = acc;
 #if FDE_SOP_TRACE
   SOP_TR(6, clock64());
