@@ -281,7 +281,7 @@ struct fde_handle_s {
   double *sop_hx = nullptr, *sop_hy = nullptr, *sop_mux = nullptr, *sop_muy = nullptr;
   double2 *sop_tw = nullptr, *sop_sc = nullptr, *sop_twA = nullptr;
   double *sop_muxL = nullptr, *sop_muyL = nullptr;
-  fde::sop::SopMaps sop_maps;                // TMA descriptors of ẑ, p̂, p̂₂ (column staging)
+  fde::sop::SopMaps sop_maps;                // TMA descriptors of ẑ, p̂, p̂₂, w_c (column staging)
   bool sop_maps_ok = false;
   const double *sop_maps_z = nullptr, *sop_maps_p = nullptr;
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
@@ -1382,7 +1382,7 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
   if (h->sop_ok) {
     const fde::sop::SopArgs sa = sop_args(h);
     if (!h->sop_maps_ok || h->sop_maps_z != h->kq || h->sop_maps_p != h->kp) {
-      FDE_CUDA(fde::sop::make_maps(&h->sop_maps, h->kq, h->kp, h->kp2, h->n, h->sine_pitch, h->batch));
+      FDE_CUDA(fde::sop::make_maps(&h->sop_maps, h->kq, h->kp, h->kp2, h->wy, h->n, h->sine_pitch, h->batch));
       h->sop_maps_ok = true;
       h->sop_maps_z = h->kq;
       h->sop_maps_p = h->kp;

@@ -52,7 +52,8 @@ cudaError_t launch(const SopArgs& a, const SopMaps& maps, cudaStream_t st) {
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-cudaError_t make_maps(SopMaps* maps, const double* z, const double* p, const double* p2, int n, int pitch, int batch) {
+cudaError_t make_maps(SopMaps* maps, const double* z, const double* p, const double* p2, const double* wc, int n,
+                      int pitch, int batch) {
   static EncodeTiledFn encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -65,9 +66,9 @@ cudaError_t make_maps(SopMaps* maps, const double* z, const double* p, const dou
   const cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)n, (cuuint64_t)batch};
   const cuuint64_t strides[2] = {(cuuint64_t)pitch * sizeof(double), (cuuint64_t)n * pitch * sizeof(double)};
   const cuuint32_t box[3] = {2, 256, 1}, estr[3] = {1, 1, 1};
-  const double* src[3] = {z, p, p2};
-  CUtensorMap* dst[3] = {&maps->z, &maps->p, &maps->p2};
-  for (int i = 0; i < 3; ++i) {
+  const double* src[4] = {z, p, p2, wc};
+  CUtensorMap* dst[4] = {&maps->z, &maps->p, &maps->p2, &maps->wc};
+  for (int i = 0; i < 4; ++i) {
     const CUresult r = encode(dst[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(src[i]), dims, strides,
                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

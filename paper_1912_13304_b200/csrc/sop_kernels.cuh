@@ -74,7 +74,7 @@ struct SopArgs {
 #define FDE_SOP_TMA 2   // 0: scattered loads; 1: ẑ by TMA, p̂_old scattered; 2: both by TMA (sequential)
 #endif
 struct alignas(64) SopMaps {
-  CUtensorMap z, p, p2;      // ẑ, p̂ buffer 0, p̂ buffer 1
+  CUtensorMap z, p, p2, wc;  // ẑ, p̂ buffer 0, p̂ buffer 1, column-direction output
 };
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
@@ -107,6 +107,17 @@ __device__ __forceinline__ void tma_columns(double2* dst, const CUtensorMap* map
   mbar_expect_tx(bar, M * 16);
 #pragma unroll
   for (int b = 0; b < M / 256; ++b) tma_load_3d(dst + 256 * b, map, c, 256 * b, rhs, bar);
+}
+
+// the unit's column pair back (rows 0..n-1; row n is clipped): one bulk group
+template <int M>
+__device__ __forceinline__ void tma_store_columns(const double2* src, const CUtensorMap* map, int c, int rhs) {
+#pragma unroll
+  for (int b = 0; b < M / 256; ++b)
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map),
+                 "r"(c), "r"(256 * b), "r"(rhs), "r"(smem_u32(src + 256 * b))
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- complex
@@ -654,7 +665,26 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const SopMaps* maps
   SOP_TR(5, clock64());
 #endif
   // ---- store the even part (chunk layout j = 16t + q, element j-1)
-  if (col) {
+  if (col && FDE_SOP_TMA) {
+    // chunk → stride layout through the padded buffer, then the dense tile
+    // (row j-1 at buf[j-1]) goes out by TMA stores (scattered 16-byte stores
+    // touched 32 cache lines per warp instruction)
+    ubar<U>(slot);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sm[G::nat(16 * t + q)] = v[q];
+    ubar<U>(slot);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = sm[G::nat(t + U * q)];
+    ubar<U>(slot);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int j = t + U * q;
+      if (j >= 1) sm[j - 1] = v[q];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes → visible to the TMA engine
+    ubar<U>(slot);
+    if (t == 0) tma_store_columns<M>(sm, &maps->wc, l0, rhs);
+  } else if (col) {
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int j = 16 * t + q;
@@ -678,7 +708,10 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const SopMaps* maps
   }
   // ---- p̂·q̂ partial of this unit (slot u); k_sine_xr5 sums them in fixed order
   double* scr = reinterpret_cast<double*>(sm + G::BUF);
-  return cta_sum2<U>(acc, scr + 40, t, slot);
+  const double tot = cta_sum2<U>(acc, scr + 40, t, slot);
+  // the TMA store has read the tile before the CTA (and its shared memory) goes away
+  if (col && FDE_SOP_TMA && t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  return tot;
 }
 
 template <int U, bool ONEWAVE>
