@@ -71,7 +71,7 @@ struct SopArgs {
 // 16-byte load per row per thread (a warp's LDG.128 then touched 32 cache
 // lines: 32 L1 tag wavefronts per instruction).
 #ifndef FDE_SOP_TMA
-#define FDE_SOP_TMA 2   // 0: scattered loads; 1: ẑ by TMA, p̂_old scattered; 2: both by TMA (sequential)
+#define FDE_SOP_TMA 1   // measurement builds: 0 = the scattered/coalesced per-thread global accesses
 #endif
 struct alignas(64) SopMaps {
   CUtensorMap z, p, p2, wc;  // ẑ, p̂ buffer 0, p̂ buffer 1, column-direction output
@@ -107,6 +107,25 @@ __device__ __forceinline__ void tma_columns(double2* dst, const CUtensorMap* map
   mbar_expect_tx(bar, M * 16);
 #pragma unroll
   for (int b = 0; b < M / 256; ++b) tma_load_3d(dst + 256 * b, map, c, 256 * b, rhs, bar);
+}
+
+// 1D bulk copies (rows are contiguous): global → shared with mbarrier
+// completion, shared → global (plain store or f64 add-reduction) in bulk groups
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_add_f64(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
 }
 
 // the unit's column pair back (rows 0..n-1; row n is clipped): one bulk group
@@ -538,16 +557,9 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const SopMaps* maps
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tma_columns<M>(sm, &maps->z, l0, rhs, bar);
     }
-    if (FDE_SOP_TMA == 1) {   // p̂_old scattered, in flight with the ẑ tile
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int j = t + U * q;
-        v[q] = __ldcg(reinterpret_cast<const double2*>(pold + base + (size_t)(j >= 1 ? j - 1 : 0) * pitch + l0));
-      }
-    }
     ubar<U>(slot);   // the barrier is initialised before anyone waits on it
     mbar_wait(bar, 0);
-    if (FDE_SOP_TMA == 2) {   // v = ẑ, then p̂_old by a second tile into the same buffer
+    {   // v = ẑ, then p̂_old by a second tile into the same buffer
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int j = t + U * q;
@@ -561,10 +573,9 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const SopMaps* maps
       mbar_wait(bar, 1);
     }
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {   // p̂ = ẑ + β p̂_old (the buffer holds p̂_old (2) or ẑ (1))
+    for (int q = 0; q < 16; ++q) {   // p̂ = ẑ + β p̂_old (the buffer holds p̂_old)
       const int j = t + U * q;
-      const double2 w = sm[j >= 1 ? j - 1 : 0];
-      const double2 zq = FDE_SOP_TMA == 2 ? v[q] : w, pq = FDE_SOP_TMA == 2 ? w : v[q];
+      const double2 pq = sm[j >= 1 ? j - 1 : 0], zq = v[q];
       const double p0 = fma(beta, pq.x, zq.x), p1 = fma(beta, pq.y, zq.y);
       v[q] = j >= 1 ? make_double2(p0, v1 ? p1 : 0.0) : make_double2(0.0, 0.0);
     }
@@ -586,6 +597,90 @@ __device__ __forceinline__ double sop_unit(const SopArgs& a, const SopMaps* maps
         v[c + i] = j >= 1 ? make_double2(p0, v1 ? p1 : 0.0) : make_double2(0.0, 0.0);
       }
     }
+  } else if (FDE_SOP_TMA) {
+    // row units: the two rows of ẑ by bulk copies into the unit's buffer (row
+    // l0 at buf[0, M), row l1 at buf[M, 2M) as doubles) while the p̂_old rows
+    // come by coalesced loads (both in flight together; p̂_old by a second
+    // bulk copy into the same buffer measured 1% slower at n = 1023);
+    // x̂ += α p̂_old by a bulk f64 add-reduction of α·p̂_old (x̂ is not
+    // loaded); p̂_new back by a bulk store. Rows are m doubles (the padding
+    // column included: p̂_new and α·p̂_old are 0 there).
+    double* const row = reinterpret_cast<double*>(sm);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(sm + G::BUF) + 56);
+    const size_t o0 = base + (size_t)l0 * pitch, o1 = base + (size_t)(v1 ? l1 : l0) * pitch;
+    const unsigned rbytes = (unsigned)(M * sizeof(double));
+    if (t == 0) {
+      mbar_init(bar);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar, v1 ? 2 * rbytes : rbytes);
+      bulk_load(row, a.z + o0, rbytes, bar);
+      if (v1) bulk_load(row + M, a.z + o1, rbytes, bar);
+    }
+    double2 qq[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int j = t + U * q, e = j >= 1 ? j - 1 : 0;
+      qq[q] = make_double2(__ldcg(pold + o0 + e), __ldcg(pold + o1 + e));
+    }
+    ubar<U>(slot);
+    mbar_wait(bar, 0);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {   // v = ẑ (stride layout, element j-1)
+      const int j = t + U * q, e = j >= 1 ? j - 1 : 0;
+      v[q] = make_double2(row[e], v1 ? row[M + e] : 0.0);
+    }
+    ubar<U>(slot);   // every thread has read ẑ: the buffer takes α p̂_old next
+    const double hy0 = a.lscale * __ldg(a.muy + l0 + 1), hy1 = v1 ? a.lscale * __ldg(a.muy + l1 + 1) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int j = t + U * q, e = j >= 1 ? j - 1 : 0;
+      const double q0 = qq[q].x, q1 = v1 ? qq[q].y : 0.0;
+      const double hx = fma(a.lscale, __ldg(a.mux + e + 1), a.nu);
+      const double p0 = fma(beta, q0, v[q].x), p1 = v1 ? fma(beta, q1, v[q].y) : 0.0;
+      if (j >= 1) {
+        acc = fma(hx + hy0, p0 * p0, acc);
+        acc = fma(hx + hy1, p1 * p1, acc);
+        row[e] = alpha * q0;          // α p̂_old, added to x̂ by the bulk reduction
+        if (v1) row[M + e] = alpha * q1;
+        v[q] = make_double2(p0, p1);
+      } else {
+        v[q] = make_double2(0.0, 0.0);
+      }
+    }
+    if (t == 0) {   // the padding column (element n = M-1) adds 0 to x̂
+      row[M - 1] = 0.0;
+      row[2 * M - 1] = 0.0;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    ubar<U>(slot);
+    if (t == 0) {
+      bulk_add_f64(a.x + o0, row, rbytes);
+      if (v1) bulk_add_f64(a.x + o1, row + M, rbytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the buffer is reused below
+    }
+    ubar<U>(slot);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {   // p̂_new rows
+      const int j = t + U * q;
+      if (j >= 1) {
+        row[j - 1] = v[q].x;
+        if (v1) row[M + j - 1] = v[q].y;
+      }
+    }
+    if (t == 0) {
+      row[M - 1] = 0.0;
+      row[2 * M - 1] = 0.0;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    ubar<U>(slot);
+    if (t == 0) {
+      bulk_store(pnew + o0, row, rbytes);
+      if (v1) bulk_store(pnew + o1, row + M, rbytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the transforms reuse the buffer
+    }
+    ubar<U>(slot);
   } else {
     const size_t o0 = base + (size_t)l0 * pitch, o1 = base + (size_t)(v1 ? l1 : l0) * pitch;
     // diagonal ν + ½λ^α_{i+1} + ½λ^β_{j+1} from the μ' tables (½λ_k = 4m² μ'_k)
