@@ -978,14 +978,17 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
     if (lane == 0) red[i * 32 + wid] = v;
   }
   __syncthreads();
-  if (threadIdx.x < 3) {
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += red[threadIdx.x * 32 + w];
-    k.part[((size_t)rhs * 3 + threadIdx.x) * KPMAX + blockIdx.x] = s;
-  }
-  __threadfence();
-  __syncthreads();
+  // thread 0 alone writes the CTA's three partials, fences and takes the
+  // ticket: the other threads do not wait for their own (large) vector
+  // stores to drain, which the finaliser does not read
   if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += red[i * 32 + w];
+      k.part[((size_t)rhs * 3 + i) * KPMAX + blockIdx.x] = s;
+    }
+    __threadfence();
     const unsigned tk = atomicAdd(&k.ctr->tickets[rhs * 8 + 1], 1u);
     s_last = (tk == gridDim.x - 1);
   }
