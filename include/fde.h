@@ -166,7 +166,10 @@ fde_status fde_measure_fp64_peak(int32_t reps, double* tflops);
  * stream (warm L2, the kernels and launch configuration the solvers use).
  * On return us[i] is the device time (µs) of the i-th kernel of that body,
  * names[i] its static name, *count the kernels per body; x and st hold the
- * stopped solve's result (status FDE_ERR_NOT_CONVERGED if maxit was hit). */
+ * stopped solve's result (status FDE_ERR_NOT_CONVERGED if maxit was hit).
+ * The 2D sine-domain operator kernel ("sine_op_sop") is replayed 5 times
+ * between its events (it leaves the solve state unchanged but for the
+ * profiled iteration's lagged x update) and us[i] is the time per launch. */
 fde_status fde_profile_solve(fde_handle h, const double* b, double* x, double rtol, int32_t maxit, int32_t solver,
                              int32_t restart, int32_t max_kernels, int32_t* count, double* us, const char** names,
                              fde_stats* st);
