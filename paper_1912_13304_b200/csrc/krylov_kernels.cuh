@@ -995,6 +995,8 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  SolveState sv;
+  if (threadIdx.x == 0) sv = k.st[rhs];
   // all threads of the last CTA sum the partials (fixed order: thread-strided
   // sums, then warps, then warp totals), loads of all slots in flight together
   __shared__ double tot[3];
@@ -1034,36 +1036,85 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
   __syncthreads();
   if (threadIdx.x != 0) return;
   k.ctr->tickets[rhs * 8 + 1] = 0u;
-  SolveState& s = k.st[rhs];
-  if (k.mode & KM_INIT) {  // start of the sine-domain PCG: ‖b̂‖ and ρ = r̂·ẑ
-    s.bnorm = sqrt(tot[1]);
-    s.rho = tot[2];
-    s.betac = 0.0;
-    s.alpha = 0.0;
-    s.kbody = 0;
-    s.ppar = 0;
-    s.iters = 0;
-    s.converged = 0;
-    s.status = ST_OK;
-    s.restarts = 0;
-    s.rnorm = 1.0;
-    if (!(s.bnorm > 0.0)) {
-      s.converged = (s.bnorm == 0.0);
-      if (!(s.bnorm == 0.0)) s.status = ST_NONFINITE;
-      s.rnorm = 0.0;
-      finish_rhs(k.ctr, s);
-    } else if (!(s.rho > 0.0)) {
-      s.status = isfinite(s.rho) ? ST_NOT_SPD : ST_NONFINITE;
-      finish_rhs(k.ctr, s);
+  // the RHS state as thread 0 prefetched it (in flight with the partial sums
+  // above), updated in registers and written back once
+  auto update = [&](SolveState& s) {
+    if (k.mode & KM_INIT) {  // start of the sine-domain PCG: ‖b̂‖ and ρ = r̂·ẑ
+      s.bnorm = sqrt(tot[1]);
+      s.rho = tot[2];
+      s.betac = 0.0;
+      s.alpha = 0.0;
+      s.kbody = 0;
+      s.ppar = 0;
+      s.iters = 0;
+      s.converged = 0;
+      s.status = ST_OK;
+      s.restarts = 0;
+      s.rnorm = 1.0;
+      if (!(s.bnorm > 0.0)) {
+        s.converged = (s.bnorm == 0.0);
+        if (!(s.bnorm == 0.0)) s.status = ST_NONFINITE;
+        s.rnorm = 0.0;
+        finish_rhs(k.ctr, s);
+      } else if (!(s.rho > 0.0)) {
+        s.status = isfinite(s.rho) ? ST_NOT_SPD : ST_NONFINITE;
+        finish_rhs(k.ctr, s);
+      }
+      return;
     }
-    return;
-  }
-  if (k.mode & KM_SROW) {
-    const int kb = s.kbody;
-    s.kbody = kb + 1;
-    if (kb >= 1) {
+    if (k.mode & KM_SROW) {
+      const int kb = s.kbody;
+      s.kbody = kb + 1;
+      if (kb >= 1) {
+        const double rn = sqrt(tot[1]);
+        s.iters = kb;
+        s.rnorm = rn / s.bnorm;
+        if (!isfinite(rn)) {
+          s.status = ST_NONFINITE;
+          finish_rhs(k.ctr, s);
+        } else if (rn <= k.rtol * s.bnorm) {
+          s.converged = 1;
+          finish_rhs(k.ctr, s);
+        } else if (kb >= k.maxit) {
+          finish_rhs(k.ctr, s);
+        }
+      }
+      if (s.cyc_active) {
+        const double rz = tot[2];
+        if (!(rz > 0.0)) {
+          s.status = isfinite(rz) ? ST_NOT_SPD : ST_NONFINITE;
+          finish_rhs(k.ctr, s);
+        } else {
+          s.betac = kb >= 1 ? rz / s.rho : 0.0;
+          s.rho = rz;
+        }
+      }
+    }
+    if (k.mode & KM_PQ) {
+      const double pq = tot[0];
+      if (!(pq > 0.0)) {
+        s.status = isfinite(pq) ? ST_NOT_SPD : ST_NONFINITE;
+        s.alpha = 0.0;  // no x update pending (the concurrent sine body lags x by one step)
+        finish_rhs(k.ctr, s);
+      } else {
+        s.alpha = s.rho / pq;
+        if (k.mode & KM_PFLIP) s.ppar ^= 1;
+      }
+    }
+    if (k.mode & KM_SOPA) {
+      const double pq = k.xval;
+      if (!(pq > 0.0)) {
+        s.status = isfinite(pq) ? ST_NOT_SPD : ST_NONFINITE;
+        s.alpha = 0.0;
+        finish_rhs(k.ctr, s);
+        return;
+      }
+      s.alpha = s.rho / pq;
+      s.ppar ^= 1;
+    }
+    if (k.mode & KM_XR) {
       const double rn = sqrt(tot[1]);
-      s.iters = kb;
+      s.iters += 1;
       s.rnorm = rn / s.bnorm;
       if (!isfinite(rn)) {
         s.status = ST_NONFINITE;
@@ -1071,67 +1122,23 @@ __device__ __forceinline__ void kry_reduce_finalize(const KryFuse& k, double (&a
       } else if (rn <= k.rtol * s.bnorm) {
         s.converged = 1;
         finish_rhs(k.ctr, s);
-      } else if (kb >= k.maxit) {
+      } else if (s.iters >= k.maxit) {
         finish_rhs(k.ctr, s);
       }
     }
-    if (s.cyc_active) {
+    if ((k.mode & KM_RZ) && s.cyc_active) {
       const double rz = tot[2];
       if (!(rz > 0.0)) {
         s.status = isfinite(rz) ? ST_NOT_SPD : ST_NONFINITE;
         finish_rhs(k.ctr, s);
       } else {
-        s.betac = kb >= 1 ? rz / s.rho : 0.0;
+        s.betac = rz / s.rho;
         s.rho = rz;
       }
     }
-  }
-  if (k.mode & KM_PQ) {
-    const double pq = tot[0];
-    if (!(pq > 0.0)) {
-      s.status = isfinite(pq) ? ST_NOT_SPD : ST_NONFINITE;
-      s.alpha = 0.0;  // no x update pending (the concurrent sine body lags x by one step)
-      finish_rhs(k.ctr, s);
-    } else {
-      s.alpha = s.rho / pq;
-      if (k.mode & KM_PFLIP) s.ppar ^= 1;
-    }
-  }
-  if (k.mode & KM_SOPA) {
-    const double pq = k.xval;
-    if (!(pq > 0.0)) {
-      s.status = isfinite(pq) ? ST_NOT_SPD : ST_NONFINITE;
-      s.alpha = 0.0;
-      finish_rhs(k.ctr, s);
-      return;
-    }
-    s.alpha = s.rho / pq;
-    s.ppar ^= 1;
-  }
-  if (k.mode & KM_XR) {
-    const double rn = sqrt(tot[1]);
-    s.iters += 1;
-    s.rnorm = rn / s.bnorm;
-    if (!isfinite(rn)) {
-      s.status = ST_NONFINITE;
-      finish_rhs(k.ctr, s);
-    } else if (rn <= k.rtol * s.bnorm) {
-      s.converged = 1;
-      finish_rhs(k.ctr, s);
-    } else if (s.iters >= k.maxit) {
-      finish_rhs(k.ctr, s);
-    }
-  }
-  if ((k.mode & KM_RZ) && s.cyc_active) {
-    const double rz = tot[2];
-    if (!(rz > 0.0)) {
-      s.status = isfinite(rz) ? ST_NOT_SPD : ST_NONFINITE;
-      finish_rhs(k.ctr, s);
-    } else {
-      s.betac = rz / s.rho;
-      s.rho = rz;
-    }
-  }
+  };
+  update(sv);
+  k.st[rhs] = sv;
 }
 
 // PREC_NONE τ step of the fused PCG: x += α p, r -= α q, z = r (‖r‖² and r·z partials)
