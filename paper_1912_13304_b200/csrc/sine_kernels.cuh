@@ -522,10 +522,18 @@ __global__ void __launch_bounds__(256, 4) k_sine_xr5(KryFuse k, int n, int lgp, 
     pv = ld4(pp + e);
   }
   {
+    // up to 16 partials per thread (nsp <= 4096 units), all loads in flight
+    // before the fixed-order sum (4 dependent round trips took ≈9 µs at n = 4095)
     const double* sp = spart + (size_t)rhs * KPMAX;
+    double pv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int ii = threadIdx.x + i * (int)blockDim.x;
+      pv[i] = ii < nsp ? __ldcg(sp + ii) : 0.0;
+    }
     double v = 0.0;
-#pragma unroll 4
-    for (int i = threadIdx.x; i < nsp; i += blockDim.x) v += __ldcg(sp + i);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v += pv[i];
     v = warp_sum(v);
     if ((threadIdx.x & 31) == 0) s_pq[threadIdx.x >> 5] = v;
     __syncthreads();
