@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(256) k_sine_init(KryFuse k, int n, int dims, c
     acc[1] = fma(rv, rv, acc[1]);
     acc[2] = fma(rv * rv, iF, acc[2]);
   })
-  if (dims == 2 && pitch > n && threadIdx.x == 0) {  // zero padding (k_sine_xr2 relies on it)
+  if (dims == 2 && pitch > n && threadIdx.x == 0) {  // zero padding (the vector steps and the p̂ tiles rely on it)
     for (int j = blockIdx.x; j < n; j += gridDim.x)
       for (int i = n; i < pitch; ++i) {
         const size_t e = o + (size_t)j * pitch + i;
