@@ -253,3 +253,166 @@ k_dstm_lines(LineArgs a) {
 }
 
 }  // namespace fde
+
+namespace fde {
+
+// log2 points per thread of the fused kernel's length-2m Toeplitz FFT (the
+// DST uses one less); must match the handle's twiddle tables (fde.cu KR, KRM)
+constexpr int KR_FUSED = 4;
+
+// ---------------------------------------------------------------------------
+// Fused right-preconditioned operator rows pass (GMRES, SURVEY §8(a) a1+a2):
+//   z  = dpost ⊙ G(dpre ⊙ x)          (TAU = false: the τ-solve's last row DST)
+//   z  = dpost ⊙ G(s ⊙ G(dpre ⊙ x))   (TAU = true: the whole 1D τ-solve)
+//   y  = ν z + cP ⊙ Sym z + cM ⊙ Skw z   (VAR) or C_μ z (!VAR; ν folded into μ)
+// for a line pair of rows, in one CTA: the DST runs on the length-m FFT
+// (k_dstm_lines' code path), z goes to global memory (the column Toeplitz pass
+// reads it) AND stays in the unit's registers as the Toeplitz input: the DST's
+// coalesced store positions e = t + P·i are exactly the Toeplitz prologue
+// positions p = (q << (K-k)) | t (both geometries have P = m/8 threads per
+// pair: 8 points per thread of the length-m FFT, 16 of the length-2m FFT), so
+// the hand-off needs no extra shared-memory round trip. One launch and one
+// pass over z fewer than DST rows → Toeplitz rows.
+// Shared memory: [Toeplitz chain: FPC·(2m+4)][DST / z staging: FPC·(m+4)][scan scratch].
+// ---------------------------------------------------------------------------
+template <int K, bool TAU, bool VAR, int FPC>
+__global__ void __launch_bounds__(FPC * (1 << (K - KR_FUSED)), min_blocks_for(FPC * (1 << (K - KR_FUSED))))
+k_dst_toep_rows(LineArgs a, double* __restrict__ zout) {
+  FDE_PDL_ENTRY();
+  constexpr int KM = K - 1, km = KR_FUSED - 1;
+  using GM = FftGeom<KM, km>;
+  using GT = FftGeom<K, KR_FUSED>;
+  using M = LineMap<GM, false, FPC>;
+  static_assert(GM::P == GT::P, "DST and Toeplitz geometries must give one thread count per pair");
+  constexpr int m = GM::L, P = GM::P, R = GM::R, C = R / 2;
+  extern __shared__ double2 smem_all[];
+  if (a.gate && *a.gate == 0) return;
+  const int f = M::group(), t = M::lane();
+  double2* smT = smem_all + (size_t)f * GT::SM_STRIDE;
+  double2* sm = smem_all + (size_t)FPC * GT::SM_STRIDE + (size_t)f * GM::SM_STRIDE;
+  double* scr = reinterpret_cast<double*>(smem_all + (size_t)FPC * (GT::SM_STRIDE + GM::SM_STRIDE));
+  const TwSrc twm{nullptr, a.twpm};
+  const TwSrc twt{nullptr, a.twp};
+  const int g = blockIdx.x * FPC + f;
+  const int l0 = 2 * g, l1 = 2 * g + 1;
+  const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
+  const Line A0 = line_of<false>(v0 ? l0 : 0, blockIdx.y, a.n, a.N), A1 = line_of<false>(v1 ? l1 : 0, blockIdx.y, a.n, a.N);
+
+  // ---- DST part (as k_dstm_lines, rows)
+  double2 vm[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int e = t + P * i;
+    if (e < m - 1) {
+      double y0 = 0.0, y1 = 0.0;
+      if (v0) y0 = __ldg(a.x + A0.base + e);
+      if (v1) y1 = __ldg(a.x + A1.base + e);
+      if (a.dpre) {
+        if (v0) y0 *= __ldg(a.dpre + A0.fbase + e);
+        if (v1) y1 *= __ldg(a.dpre + A1.fbase + e);
+      }
+      sm[GM::swz(e)] = make_double2(y0, y1);
+    }
+  }
+  __syncthreads();
+  dstm_pre_smem<GM, KM, km>(vm, sm, t, a.sinm);
+  dif_chain<GM, -1, false>(vm, sm, t, twm);
+  double g0[R], g1[R];
+  dstm_post<GM, false, FPC>(vm, sm, scr, t, f, g0, g1);
+  if (TAU) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int idx = 2 * C * t + i;
+      if (idx < 1) continue;
+      const double s = a.invF[idx - 1];
+      sm[GM::swz(idx - 1)] = make_double2(s * g0[i], s * g1[i]);
+    }
+    __syncthreads();
+    dstm_pre_smem<GM, KM, km>(vm, sm, t, a.sinm);
+    dif_chain<GM, -1, false>(vm, sm, t, twm);
+    dstm_post<GM, false, FPC>(vm, sm, scr, t, f, g0, g1);
+  }
+  // z: chunk layout → natural order through shared memory, coalesced stores;
+  // the scaled z stays in sm (natural order) for the ν z term and in v as the
+  // Toeplitz input (v[q] at p = q·P + t, the store position of register q)
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    if (2 * C * t + i >= 1) sm[GM::swz(2 * C * t + i - 1)] = make_double2(g0[i], g1[i]);
+  __syncthreads();
+  double2 v[GT::R];
+  const double osc = a.oscale != 0.0 ? a.oscale : 1.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int e = t + P * i;
+    double z0 = 0.0, z1 = 0.0;
+    if (e < m - 1) {
+      const double2 o = sm[GM::swz(e)];
+      z0 = o.x * osc;
+      z1 = o.y * osc;
+      if (a.dpost) {
+        z0 *= __ldg(a.dpost + A0.fbase + e);
+        z1 *= __ldg(a.dpost + A1.fbase + e);
+      }
+      if (!v0) z0 = 0.0;
+      if (!v1) z1 = 0.0;
+      if (v0) zout[A0.base + e] = z0;
+      if (v1) zout[A1.base + e] = z1;
+      sm[GM::swz(e)] = make_double2(z0, z1);
+    }
+    v[i] = make_double2(z0, z1);
+  }
+#pragma unroll
+  for (int q = GT::R / 2; q < GT::R; ++q) v[q] = make_double2(0.0, 0.0);
+
+  // ---- Toeplitz part (as k_toeplitz_lines, rows, no Krylov hooks)
+  dif_chain<GT, -1, true>(v, smT, t, twt);
+  double2 u[GT::R / 2];
+  if (!VAR) {
+#pragma unroll
+    for (int q = 0; q < GT::R; ++q) v[q] = c_mul(v[q], a.mu[q * GT::P + t]);
+    dit_chain<GT, +1>(v, smT, t, twt);
+  } else {
+    double2* zs = a.zscr + ((size_t)(blockIdx.y * gridDim.x) * FPC + g) * GT::L;
+#pragma unroll
+    for (int q = 0; q < GT::R; ++q) {
+      zs[q * GT::P + t] = v[q];
+      v[q] = c_scale(v[q], a.lamS[q * GT::P + t]);
+    }
+    dit_chain<GT, +1>(v, smT, t, twt);
+#pragma unroll
+    for (int q = 0; q < GT::R / 2; ++q) u[q] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < GT::R; ++q) {
+      const double2 z = zs[q * GT::P + t];
+      const double lk = a.lamK[q * GT::P + t];
+      v[q] = make_double2(-lk * z.y, lk * z.x);
+    }
+    dit_chain<GT, +1>(v, smT, t, twt);
+  }
+#pragma unroll
+  for (int q = 0; q < GT::R / 2; ++q) {
+    const int p = (q << (K - KR_FUSED)) | t;
+    if (p >= a.n) continue;
+    const int f0 = A0.fbase + p, f1 = A1.fbase + p;
+    double r0, r1;
+    if (!VAR) {
+      r0 = v[q].x;
+      r1 = v[q].y;
+    } else {
+      r0 = v0 ? __ldg(a.cP + f0) * u[q].x + __ldg(a.cM + f0) * v[q].x : 0.0;
+      r1 = v1 ? __ldg(a.cP + f1) * u[q].y + __ldg(a.cM + f1) * v[q].y : 0.0;
+    }
+    if (a.nu != 0.0) {
+      const double2 zz = sm[GM::swz(p)];
+      r0 = fma(a.nu, zz.x, r0);
+      r1 = fma(a.nu, zz.y, r1);
+    }
+    if (v0) a.y[A0.base + p] = r0;
+    if (v1) a.y[A1.base + p] = r1;
+  }
+}
+
+}  // namespace fde

@@ -217,6 +217,20 @@ struct LaunchCfgM {
   static constexpr int SMEM = FPC * SPG + SCR;
 };
 
+// fused τ-DST + Toeplitz rows kernel (dst_kernels.cuh k_dst_toep_rows)
+template <int K>
+struct LaunchCfgF {
+  using GT = FftGeom<K, KR>;
+  using GM = FftGeom<K - 1, KRM>;
+  static constexpr int P = GT::P;
+  static constexpr int FPC = 128 / P > 1 ? 128 / P : 1;   // ~128 threads per CTA, as the rows passes
+  static constexpr int THREADS = FPC * P;
+  static constexpr int SCR = (FPC * (GroupScan<false, GM::P, FPC>::NSEG + 1) * 2) * 8;
+  static constexpr int SMEM = FPC * (GT::SM_STRIDE + GM::SM_STRIDE) * 16 + SCR;
+  static constexpr bool FITS = SMEM <= 227 * 1024;
+};
+static_assert(KR == KR_FUSED && KRM == KR_FUSED - 1, "k_dst_toep_rows uses the handle's twiddle tables");
+
 // sine-domain operator kernels (sine_kernels.cuh)
 template <int KM, bool COL, int MODE>
 struct LaunchCfgS {
@@ -482,6 +496,13 @@ void init_kernel_attrs() {
   FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, false, D0::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0::SMEM));
   FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, true, D1::FPC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D1::SMEM));
   FDE_CUDA(cudaFuncSetAttribute(k_dstm_lines<K - 1, KRM, true, D1::FPC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, D1::SMEM));
+  using F = LaunchCfgF<K>;
+  if (F::FITS) {
+    FDE_CUDA(cudaFuncSetAttribute(k_dst_toep_rows<K, false, false, F::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM));
+    FDE_CUDA(cudaFuncSetAttribute(k_dst_toep_rows<K, false, true, F::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM));
+    FDE_CUDA(cudaFuncSetAttribute(k_dst_toep_rows<K, true, false, F::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM));
+    FDE_CUDA(cudaFuncSetAttribute(k_dst_toep_rows<K, true, true, F::FPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM));
+  }
 }
 
 // One Toeplitz pass along rows (COL=false) or columns (COL=true).
@@ -737,6 +758,78 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate, const Kry
   c.y = z;
   c.dpost = h->dpost;
   FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, c)));
+}
+
+// y = A P⁻¹ v with z = P⁻¹ v also written (the right-preconditioned GMRES
+// operator, a2 then a1). FFT path with a τ kind: the τ-solve's last row DST
+// (2D) or the whole 1D τ-solve runs in the same kernel as the row Toeplitz
+// pass (k_dst_toep_rows): 2D = rows DST, columns τ core, rows [DST, Toeplitz],
+// columns Toeplitz (4 launches instead of 5); 1D = one launch instead of 2.
+template <int K, bool TAU, bool VAR>
+void launch_dst_toep_k(fde_handle h, const LineArgs& a, double* zout) {
+  using F = LaunchCfgF<K>;
+  const int npairs = (a.nlines + 1) / 2;
+  const dim3 grid((npairs + F::FPC - 1) / F::FPC, h->batch);
+  launch_named(h, TAU ? "tau_toeplitz_rows" : (VAR ? "dst_toeplitz_rows_var" : "dst_toeplitz_rows"),
+               [&] { launch_k(h->st, k_dst_toep_rows<K, TAU, VAR, F::FPC>, grid, F::THREADS, F::SMEM, a, zout); });
+}
+template <int K>
+constexpr bool dst_toep_fits() { return LaunchCfgF<K>::FITS; }
+
+void op_tau_matvec(fde_handle h, const double* v, double* z, double* y, const int* gate) {
+  const bool tau = h->d.prec == FDE_PREC_TAU || h->d.prec == FDE_PREC_TAU_D || h->d.prec == FDE_PREC_TAU_DSYM;
+  bool fits = false;
+  if (!h->dense && tau) { FDE_SWITCH_K(h->K, (fits = dst_toep_fits<KK>())); }
+  if (!fits) {
+    op_tau(h, v, z, gate);
+    op_matvec(h, z, y, gate);
+    return;
+  }
+  // the row pass's arguments: the Toeplitz part as toeplitz_pass sets them
+  LineArgs c = base_args(h);
+  c.gate = gate;
+  c.nlines = h->dims == 1 ? 1 : h->n;
+  c.y = h->dims == 1 ? y : h->wx;
+  c.dpost = h->dpost;
+  const bool var = h->var_x;
+  if (!var) {
+    c.mu = h->mu_x;
+    c.nu = 0.0;  // folded into μ_x
+  } else {
+    c.lamS = h->lamS_x;
+    c.lamK = h->lamK_x;
+    c.cP = h->cP_x;
+    c.cM = h->cM_x;
+    c.nu = h->d.nu;
+  }
+  if (h->dims == 1) {
+    c.x = v;
+    c.invF = h->invF;
+    c.dpre = h->dpre;
+    if (var) { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, true, true>(h, c, z))); }
+    else { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, true, false>(h, c, z))); }
+    return;
+  }
+  LineArgs a = base_args(h);
+  a.gate = gate;
+  a.nlines = h->n;
+  a.x = v;
+  a.y = h->t1;
+  a.dpre = h->dpre;
+  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, a)));
+  LineArgs b = base_args(h);
+  b.gate = gate;
+  b.nlines = h->n;
+  b.x = h->t1;
+  b.y = h->t2;
+  b.Fx = h->Fx;
+  b.Fy = h->Fy;
+  b.fscale = h->fscale;
+  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, true, true>(h, b)));
+  c.x = h->t2;
+  if (var) { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, false, true>(h, c, z))); }
+  else { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, false, false>(h, c, z))); }
+  toeplitz_pass(h, true, z, y, h->wx, 0.0, gate);
 }
 
 // ------------------------------------------------------------- create
@@ -1577,8 +1670,7 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
       }
       double* Vn = V + (size_t)(j + 1) * vs;
       if (!left) {
-        op_tau(h, Vj, h->kz, gA);
-        op_matvec(h, h->kz, Vn, gA);
+        op_tau_matvec(h, Vj, h->kz, Vn, gA);
       } else {
         op_matvec(h, Vj, h->kq, gA);
         op_tau(h, h->kq, Vn, gA);
@@ -1604,8 +1696,7 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
     double* Vj = V + (size_t)j * vs;
     double* Vn = V + (size_t)(j + 1) * vs;
     if (!left) {
-      op_tau(h, Vj, h->kz, gA);
-      op_matvec(h, h->kz, Vn, gA);
+      op_tau_matvec(h, Vj, h->kz, Vn, gA);
     } else {
       op_matvec(h, Vj, h->kq, gA);
       op_tau(h, h->kq, Vn, gA);
