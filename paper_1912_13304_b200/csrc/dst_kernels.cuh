@@ -298,15 +298,20 @@ k_dst_toep_rows(LineArgs a, double* __restrict__ zout) {
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
   const Line A0 = line_of<false>(v0 ? l0 : 0, blockIdx.y, a.n, a.N), A1 = line_of<false>(v1 ? l1 : 0, blockIdx.y, a.n, a.N);
 
-  // ---- DST part (as k_dstm_lines, rows)
+  // ---- DST part (as k_dstm_lines, rows); the input rows have pitch a.pitch
+  //      (0 = n: the user layout; m: the stau output t2)
+  const int xp = a.pitch ? a.pitch : a.n;
+  const long long xrhs = a.pitch ? (long long)a.n * a.pitch : (long long)a.N;   // per-RHS stride (1D: N = n)
+  const long long xb0 = (long long)blockIdx.y * xrhs + (long long)(v0 ? l0 : 0) * xp;
+  const long long xb1 = (long long)blockIdx.y * xrhs + (long long)(v1 ? l1 : 0) * xp;
   double2 vm[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int e = t + P * i;
     if (e < m - 1) {
       double y0 = 0.0, y1 = 0.0;
-      if (v0) y0 = __ldg(a.x + A0.base + e);
-      if (v1) y1 = __ldg(a.x + A1.base + e);
+      if (v0) y0 = __ldg(a.x + xb0 + e);
+      if (v1) y1 = __ldg(a.x + xb1 + e);
       if (a.dpre) {
         if (v0) y0 *= __ldg(a.dpre + A0.fbase + e);
         if (v1) y1 *= __ldg(a.dpre + A1.fbase + e);

@@ -297,6 +297,11 @@ struct fde_handle_s {
   double2 *sop_tw = nullptr, *sop_sc = nullptr, *sop_twA = nullptr;
   double *sop_muxL = nullptr, *sop_muyL = nullptr;
   fde::sop::SopMaps sop_maps;                // TMA descriptors of ẑ, p̂, p̂₂, w_c (column staging)
+  // 2D τ-solve on the r02 transform engine (stau_kernels.cuh): rows DST,
+  // columns τ core on t1/t2 at pitch m (TMA), for m in {512..4096} and a τ kind
+  bool stau_ok = false;
+  double* stau_FyL = nullptr;                // lane-major cy·F_β: FyL[q·U + t] = Fy[16t + q - 1]
+  fde::sop::StauMaps stau_maps;
   bool sop_maps_ok = false;
   const double *sop_maps_z = nullptr, *sop_maps_p = nullptr;
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
@@ -689,6 +694,36 @@ void op_copy(fde_handle h, const double* src, double* dst) {
   launch_named(h, "copy", [&] { launch_k(h->st, k_copy, 592, 256, 0, src, dst, n); });
 }
 
+// 2D τ-solve passes on the r02 transform engine (stau_kernels.cuh)
+fde::sop::StauArgs stau_args(fde_handle h, const int* gate) {
+  fde::sop::StauArgs sa{};
+  sa.n = h->n;
+  sa.m = h->m;
+  sa.FyL = h->stau_FyL;
+  sa.Fx = h->Fx;
+  sa.fscale = h->fscale;
+  sa.tw = h->sop_tw;
+  sa.twA = h->sop_twA;
+  sa.sc = h->sop_sc;
+  sa.gate = gate;
+  return sa;
+}
+void stau_rows(fde_handle h, const double* x, int xp, double* y, int yp, const double* dpre, const double* dpost,
+               const int* gate) {
+  fde::sop::StauArgs sa = stau_args(h, gate);
+  sa.x = x;
+  sa.y = y;
+  sa.xp = xp;
+  sa.yp = yp;
+  sa.dpre = dpre;
+  sa.dpost = dpost;
+  launch_named(h, "stau_rows", [&] { FDE_CUDA(fde::sop::stau_launch(false, sa, nullptr, h->batch, h->st)); });
+}
+void stau_cols(fde_handle h, const int* gate) {   // t1 → t2 (pitch m)
+  const fde::sop::StauArgs sa = stau_args(h, gate);
+  launch_named(h, "stau_cols", [&] { FDE_CUDA(fde::sop::stau_launch(true, sa, &h->stau_maps, h->batch, h->st)); });
+}
+
 // z = P⁻¹ r (a2). With kf (fused PCG): the first kernel forms r -= αq,
 // x += αp (KM_XR, r is read from kf->r) and the last accumulates r·z (KM_RZ).
 void op_tau(fde_handle h, const double* r, double* z, const int* gate, const KryFuse* kf = nullptr) {
@@ -735,6 +770,12 @@ void op_tau(fde_handle h, const double* r, double* z, const int* gate, const Kry
     return;
   }
   // 2D: rows DST (pre-scale) -> columns DST·F⁻¹·DST -> rows DST (post-scale)
+  if (h->stau_ok && !kf) {
+    stau_rows(h, r, h->n, h->t1, h->m, h->dpre, nullptr, gate);
+    stau_cols(h, gate);
+    stau_rows(h, h->t2, h->m, z, h->n, nullptr, h->dpost, gate);
+    return;
+  }
   a.nlines = h->n;
   a.x = r;
   a.y = h->t1;
@@ -810,23 +851,31 @@ void op_tau_matvec(fde_handle h, const double* v, double* z, double* y, const in
     else { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, true, false>(h, c, z))); }
     return;
   }
-  LineArgs a = base_args(h);
-  a.gate = gate;
-  a.nlines = h->n;
-  a.x = v;
-  a.y = h->t1;
-  a.dpre = h->dpre;
-  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, a)));
-  LineArgs b = base_args(h);
-  b.gate = gate;
-  b.nlines = h->n;
-  b.x = h->t1;
-  b.y = h->t2;
-  b.Fx = h->Fx;
-  b.Fy = h->Fy;
-  b.fscale = h->fscale;
-  FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, true, true>(h, b)));
+  int xpitch = h->n;
+  if (h->stau_ok) {
+    stau_rows(h, v, h->n, h->t1, h->m, h->dpre, nullptr, gate);
+    stau_cols(h, gate);
+    xpitch = h->m;
+  } else {
+    LineArgs a = base_args(h);
+    a.gate = gate;
+    a.nlines = h->n;
+    a.x = v;
+    a.y = h->t1;
+    a.dpre = h->dpre;
+    FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, false, false>(h, a)));
+    LineArgs b = base_args(h);
+    b.gate = gate;
+    b.nlines = h->n;
+    b.x = h->t1;
+    b.y = h->t2;
+    b.Fx = h->Fx;
+    b.Fy = h->Fy;
+    b.fscale = h->fscale;
+    FDE_SWITCH_K(h->K, (launch_dstm_k<KK - 1, true, true>(h, b)));
+  }
   c.x = h->t2;
+  c.pitch = xpitch;
   if (var) { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, false, true>(h, c, z))); }
   else { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, false, false>(h, c, z))); }
   toeplitz_pass(h, true, z, y, h->wx, 0.0, gate);
@@ -1010,6 +1059,21 @@ void build(fde_handle h, const fde_desc* d) {
     h->sop_muy = h->upload(muy);
     h->sop_hx = h->upload(hx);
     h->sop_hy = h->upload(hy);
+    const int U = m / 16;
+    std::vector<double> muxL(m + 1), muyL(m + 1);
+    for (int t = 0; t < U; ++t)
+      for (int q = 0; q < 16; ++q) {
+        muxL[q * U + t] = mux[16 * t + q];
+        muyL[q * U + t] = muy[16 * t + q];
+      }
+    muxL[m] = mux[m];
+    muyL[m] = muy[m];
+    h->sop_muxL = h->upload(muxL);
+    h->sop_muyL = h->upload(muyL);
+  }
+  h->stau_ok = two && !h->dense && fde::sop::supported(m) &&
+               (d->prec == FDE_PREC_TAU || d->prec == FDE_PREC_TAU_D || d->prec == FDE_PREC_TAU_DSYM);
+  if (h->sop_ok || h->stau_ok) {  // transform tables of the r02 engine (sop_kernels.cuh transform<U>)
     std::vector<double2> tw(m / 2), sc(m / 16);
     for (int e = 0; e < m / 2; ++e) {
       const auto z = root_of_unity(e, m);
@@ -1026,17 +1090,7 @@ void build(fde_handle h, const fde_desc* d) {
     std::vector<double2> twA(4 * U);
     for (int i = 0; i < 4; ++i)
       for (int t = 0; t < U; ++t) twA[i * U + t] = tw[(size_t)t << i];
-    std::vector<double> muxL(m + 1), muyL(m + 1);
-    for (int t = 0; t < U; ++t)
-      for (int q = 0; q < 16; ++q) {
-        muxL[q * U + t] = mux[16 * t + q];
-        muyL[q * U + t] = muy[16 * t + q];
-      }
-    muxL[m] = mux[m];
-    muyL[m] = muy[m];
     h->sop_twA = h->upload(twA);
-    h->sop_muxL = h->upload(muxL);
-    h->sop_muyL = h->upload(muyL);
   }
 
   // preconditioner tables
@@ -1102,6 +1156,16 @@ void build(fde_handle h, const fde_desc* d) {
       h->Fx = h->upload(Fa);
       h->Fy = h->upload(Fb);
       h->fscale = 1.0 / ((2.0 * m) * (2.0 * m));
+      if (h->stau_ok) {  // lane-major Fy for the stau column units (chunk layout j = 16t + q, row j-1)
+        const int U = m / 16;
+        std::vector<double> fl(m, 0.0);
+        for (int t = 0; t < U; ++t)
+          for (int q = 0; q < 16; ++q) {
+            const int j = 16 * t + q;
+            fl[q * U + t] = j >= 1 ? Fb[j - 1] : 1.0;
+          }
+        h->stau_FyL = h->upload(fl);
+      }
     }
     if (prec == FDE_PREC_TAU_D || prec == FDE_PREC_TAU_DSYM) {
       std::vector<double> D(N);
@@ -1129,6 +1193,7 @@ void build(fde_handle h, const fde_desc* d) {
   h->t1 = h->dalloc<double>(ve);
   h->t2 = h->dalloc<double>(ve);
   h->t3 = h->dalloc<double>(ve);
+  if (h->stau_ok) FDE_CUDA(fde::sop::make_stau_maps(&h->stau_maps, h->t1, h->t2, n, h->batch));
   h->hin = h->dalloc<double>(ve);
   h->hout = h->dalloc<double>(ve);
   h->sst = h->dalloc<SolveState>(h->batch);

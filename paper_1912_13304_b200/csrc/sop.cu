@@ -4,6 +4,7 @@
 
 #include "sop.h"
 #include "sop_kernels.cuh"
+#include "stau_kernels.cuh"
 
 namespace fde {
 namespace sop {
@@ -78,6 +79,43 @@ cudaError_t make_maps(SopMaps* maps, const double* z, const double* p, const dou
 }
 
 int warps_for(int m, int batch) { return batch * m; }   // units (CTAs): 2·npairs = m per RHS
+
+// ---- 2D τ-solve on the r02 transform engine (stau_kernels.cuh)
+template <int U>
+static cudaError_t stau_k(bool cols, const StauArgs& a, const StauMaps* maps, int batch, cudaStream_t st) {
+  const size_t smem = (size_t)Geo<U>::SLOTS * sizeof(double2);
+  const dim3 grid((a.n + 1) / 2, batch);
+  if (cols) {
+    cudaError_t e = cudaFuncSetAttribute(k_stau_cols<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_stau_cols<U><<<grid, U, smem, st>>>(a, *maps);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(k_stau_rows<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_stau_rows<U><<<grid, U, smem, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t stau_launch(bool cols, const StauArgs& a, const StauMaps* maps, int batch, cudaStream_t st) {
+  switch (a.m) {
+    case 512: return stau_k<32>(cols, a, maps, batch, st);
+    case 1024: return stau_k<64>(cols, a, maps, batch, st);
+    case 2048: return stau_k<128>(cols, a, maps, batch, st);
+    case 4096: return stau_k<256>(cols, a, maps, batch, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t make_stau_maps(StauMaps* maps, const double* t1, const double* t2, int n, int batch) {
+  SopMaps tmp;
+  // the same descriptor shape as the sop column staging: [batch][n][m], box 2 × 256
+  cudaError_t e = make_maps(&tmp, t1, t2, t1, t2, n, n + 1, batch);
+  if (e != cudaSuccess) return e;
+  maps->t1 = tmp.z;
+  maps->t2 = tmp.p;
+  return cudaSuccess;
+}
 
 }  // namespace sop
 }  // namespace fde

@@ -67,7 +67,7 @@ CASES = [
     (2, 2047, 1, W.PREC_TAU_D), (2, 4095, 1, W.PREC_TAU_D), (2, 4095, 2, W.PREC_TAU_DSYM),
     (3, 31, 1, W.PREC_TAU), (3, 63, 3, W.PREC_TAU), (3, 511, 1, W.PREC_TAU),
     (4, 63, 1, W.PREC_TAU), (4, 127, 2, W.PREC_TAU), (4, 255, 1, W.PREC_TAU_D), (4, 255, 3, W.PREC_TAU_DSYM),
-    (4, 1023, 1, W.PREC_TAU), (4, 1023, 2, W.PREC_TAU_D),
+    (4, 1023, 1, W.PREC_TAU), (4, 1023, 2, W.PREC_TAU_D), (4, 511, 3, W.PREC_TAU_DSYM), (3, 2047, 1, W.PREC_TAU_D),
     (5, 255, 8, W.PREC_TAU), (5, 1023, 1, W.PREC_TAU), (5, 2047, 1, W.PREC_TAU),
 ]
 

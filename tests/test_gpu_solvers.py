@@ -59,6 +59,7 @@ SOLVES = [
     (3, 63, 2, "pcg", W.PREC_TAU), (3, None, 1, "pcg", W.PREC_TAU),
     (3, 63, 1, "gmres", W.PREC_TAU), (3, 127, 2, "gmres", W.PREC_TAU_DSYM),
     (4, 63, 1, "gmres", W.PREC_TAU), (4, 127, 2, "gmres", W.PREC_TAU_D), (4, 255, 1, "gmres", W.PREC_TAU),
+    (4, 511, 1, "gmres", W.PREC_TAU_DSYM), (3, 511, 2, "gmres", W.PREC_TAU_D),
     (5, 255, 4, "pcg", W.PREC_TAU),
 ]
 
