@@ -12,7 +12,10 @@ namespace sop {
 template <int U, bool ONEWAVE>
 static cudaError_t launch_k(const SopArgs& a, const SopMaps& maps, cudaStream_t st) {
   constexpr int UPC = sop_upc<U>();
-  const size_t smem = (size_t)UPC * Geo<U>::SLOTS * sizeof(double2);
+#ifndef FDE_SOP_SMEM_PAD
+#define FDE_SOP_SMEM_PAD 0   // measurement builds only: extra dynamic smem per CTA (limits units per SM)
+#endif
+  const size_t smem = (size_t)UPC * Geo<U>::SLOTS * sizeof(double2) + FDE_SOP_SMEM_PAD;
   auto kern = k_sop<U, ONEWAVE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
