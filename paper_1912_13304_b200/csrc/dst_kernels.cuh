@@ -298,6 +298,7 @@ k_dst_toep_rows(LineArgs a, double* __restrict__ zout) {
   const bool v0 = l0 < a.nlines, v1 = l1 < a.nlines;
   const Line A0 = line_of<false>(v0 ? l0 : 0, blockIdx.y, a.n, a.N), A1 = line_of<false>(v1 ? l1 : 0, blockIdx.y, a.n, a.N);
 
+  if (VAR) prefetch_coef_rows(a, A0, v0, v1, t);
   // ---- DST part (as k_dstm_lines, rows); the input rows have pitch a.pitch
   //      (0 = n: the user layout; m: the stau output t2)
   const int xp = a.pitch ? a.pitch : a.n;

@@ -566,7 +566,11 @@ __global__ void __launch_bounds__(256) k_gm_cgs_ws(VecArgs a, const double* __re
 // order at both levels (deterministic); the serial tail is two short rounds
 // instead of one block summing nvec × gridDim.x partials.
 constexpr int RGS = 16;
-__device__ __forceinline__ bool finalize2(const VecArgs& a, int rb, const double* part, int nvec, double* out) {
+// level 1 and the final ticket: true for the launch's finalising block (the
+// group sums of every vector are then in gpart, visible to it). Four threads
+// per vector, four partials each, all loads in flight; the four are combined
+// by two butterfly shuffles (a fixed order: deterministic).
+__device__ __forceinline__ bool finalize2_l1(const VecArgs& a, int rb, const double* part, int nvec) {
   __shared__ bool s_l;
   const int G = (int)gridDim.x, grp = blockIdx.x / RGS, ngrp = (G + RGS - 1) / RGS;
   const int gcnt = min(RGS, G - grp * RGS);
@@ -578,14 +582,18 @@ __device__ __forceinline__ bool finalize2(const VecArgs& a, int rb, const double
   __threadfence();
   if (threadIdx.x == 0) a.ctr->gtickets[rb * 64 + grp] = 0u;
   double* gp = a.gpart + (size_t)rb * 64 * 64;
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-    double v[RGS];
+  for (int q0 = 0; q0 < nvec * 4; q0 += blockDim.x) {
+    const int q = q0 + threadIdx.x, i = q >> 2, sub = q & 3;
+    double v[4];
 #pragma unroll
-    for (int b = 0; b < RGS; ++b) v[b] = b < gcnt ? __ldcg(part + (size_t)i * RED_BLOCKS + grp * RGS + b) : 0.0;
-    double sum = 0.0;
-#pragma unroll
-    for (int b = 0; b < RGS; ++b) sum += v[b];
-    gp[i * 64 + grp] = sum;
+    for (int b = 0; b < 4; ++b) {
+      const int bb = sub * 4 + b;
+      v[b] = (i < nvec && bb < gcnt) ? __ldcg(part + (size_t)i * RED_BLOCKS + grp * RGS + bb) : 0.0;
+    }
+    double sum = (v[0] + v[1]) + (v[2] + v[3]);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    if (i < nvec && sub == 0) gp[i * 64 + grp] = sum;
   }
   __threadfence();
   __syncthreads();
@@ -594,59 +602,95 @@ __device__ __forceinline__ bool finalize2(const VecArgs& a, int rb, const double
   if (!s_l) return false;
   __threadfence();
   if (threadIdx.x == 0) a.ctr->tickets[rb * 8] = 0u;
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
-    double v[8];
-    double sum = 0.0;
-    for (int g0 = 0; g0 < ngrp; g0 += 8) {
-#pragma unroll
-      for (int g = 0; g < 8; ++g) v[g] = g0 + g < ngrp ? __ldcg(gp + i * 64 + g0 + g) : 0.0;
-#pragma unroll
-      for (int g = 0; g < 8; ++g) sum += v[g];
-    }
-    out[i] = sum;
-  }
-  __syncthreads();
   return true;
 }
+// level 2 (the finalising block): the <= 40 group sums of every vector, four
+// threads per vector with ten loads each in flight, into sh[0 .. nvec)
+// (shared memory; the caller synchronises)
+static_assert((RED_BLOCKS + RGS - 1) / RGS <= 40, "finalize2_l2 sums at most 40 groups");
+__device__ __forceinline__ void finalize2_l2(const VecArgs& a, int rb, int nvec, double* sh) {
+  const int ngrp = ((int)gridDim.x + RGS - 1) / RGS;
+  const double* gp = a.gpart + (size_t)rb * 64 * 64;
+  for (int q0 = 0; q0 < nvec * 4; q0 += blockDim.x) {
+    const int q = q0 + threadIdx.x, i = q >> 2, sub = q & 3;
+    double v[10];
+#pragma unroll
+    for (int g = 0; g < 10; ++g) {
+      const int gg = sub * 10 + g;
+      v[g] = (i < nvec && gg < ngrp) ? __ldcg(gp + i * 64 + gg) : 0.0;
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int g = 0; g < 10; ++g) sum += v[g];
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    if (i < nvec && sub == 0) sh[i] = sum;
+  }
+}
 
-// the finalising block of pass A (all its threads; sums in gs.h[0 .. 2j+1]):
+// the finalising block of pass A (all its threads; the group sums are in gpart):
 // thread 0 finalises column j-1 (O(j) serial, on register copies), the
 // block forms the new raw column j in parallel
 __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z) {
   SolveState& s = a.st[rb];
   GmresSmall& gs = a.gs[rb];
   constexpr int LD = MAX_RESTART + 1;
-  __shared__ double sa[32], sb[32], scs[32], ssn[32], scol[33];
-  __shared__ double s_bet, s_nu, s_g;
-  __shared__ int s_stop;
-  // every operand of the serial part is fetched in parallel first (one round trip)
-  for (int i = threadIdx.x; i < 32; i += blockDim.x) {
-    if (i < j) {
-      sa[i] = __ldcg(&gs.h[i]);
-      sb[i] = __ldcg(&gs.h[j + i]);
-      scol[i] = __ldcg(&gs.Hr[(size_t)(j - 1) * LD + i]);
-    }
-    if (i + 1 < j) {
-      scs[i] = __ldcg(&gs.cs[i]);
-      ssn[i] = __ldcg(&gs.sn[i]);
-    }
+  __shared__ double s_h[64], scs[32], ssn[32], scol[33];
+  __shared__ double s_bet, s_g, s_bnorm;
+  __shared__ int s_stop, s_iters, s_act;
+  __shared__ double sHr[32 * 33];   // DCGS2 runs for restart <= 31
+  // ONE round trip for everything the serial part reads: the operands go to
+  // registers first, then the level-2 loads of this pass's sums (a at 0..,
+  // b at j.., ν at 2j, c at 2j+1) are issued, then all of it lands in shared
+  // memory. sHr: the finalised raw columns k < j-1 (upper Hessenberg: rows
+  // i <= k+1) for the H·a products of the parallel part (read from global
+  // memory there they were ≈ j/4 dependent L2 round trips).
+  const int tx = threadIdx.x, bd = blockDim.x;
+  double o_col = 0.0, o_cs = 0.0, o_sn = 0.0, o_g = 0.0, o_bn = 0.0;
+  int o_it = 0, o_act = 0;
+  if (tx < j && tx < 32) o_col = __ldcg(&gs.Hr[(size_t)(j - 1) * LD + tx]);
+  if (tx + 1 < j && tx < 32) {
+    o_cs = __ldcg(&gs.cs[tx]);
+    o_sn = __ldcg(&gs.sn[tx]);
   }
-  // (any block size: the passes run with 32..256 threads); the RHS state the
-  // serial part reads is fetched here too, so thread 0 issues no load of its own
-  __shared__ double s_bnorm, s_cc;
-  __shared__ int s_iters, s_act;
-  if (threadIdx.x == (32 % blockDim.x)) s_nu = __ldcg(&gs.h[2 * j]);
-  if (threadIdx.x == (64 % blockDim.x) && j >= 1) s_g = __ldcg(&gs.g[j - 1]);
-  if (threadIdx.x == (96 % blockDim.x)) s_bnorm = __ldcg(&s.bnorm);
-  if (threadIdx.x == (128 % blockDim.x)) s_iters = __ldcg(&s.iters);
-  if (threadIdx.x == (160 % blockDim.x)) s_act = __ldcg(&s.cyc_active);
-  if (threadIdx.x == (192 % blockDim.x)) s_cc = has_z ? __ldcg(&gs.h[2 * j + 1]) : 0.0;
+  if (tx == (64 % bd) && j >= 1) o_g = __ldcg(&gs.g[j - 1]);
+  if (tx == (96 % bd)) o_bn = __ldcg(&s.bnorm);
+  if (tx == (128 % bd)) o_it = __ldcg(&s.iters);
+  if (tx == (160 % bd)) o_act = __ldcg(&s.cyc_active);
+  const int nhr = has_z ? (j - 1) * 32 : 0;
+  double hr[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int q = tx + u * bd, k = q >> 5, i = q & 31;
+    hr[u] = (q < nhr && i <= k + 1) ? __ldcg(&gs.Hr[(size_t)k * LD + i]) : 0.0;
+  }
+  finalize2_l2(a, rb, 2 * j + 2, s_h);
+  const double* sa = s_h;
+  const double* sb = s_h + j;
+  if (tx < 32) {
+    scol[tx] = o_col;
+    scs[tx] = o_cs;
+    ssn[tx] = o_sn;
+  }
+  if (tx == (64 % bd)) s_g = o_g;
+  if (tx == (96 % bd)) s_bnorm = o_bn;
+  if (tx == (128 % bd)) s_iters = o_it;
+  if (tx == (160 % bd)) s_act = o_act;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int q = tx + u * bd;
+    if (q < nhr) sHr[(q >> 5) * 33 + (q & 31)] = hr[u];
+  }
+  for (int q = tx + 4 * bd; q < nhr; q += bd) {   // block sizes below 256
+    const int k = q >> 5, i = q & 31;
+    if (i <= k + 1) sHr[k * 33 + i] = __ldcg(&gs.Hr[(size_t)k * LD + i]);
+  }
   __syncthreads();
 #if FDE_SOP_TRACE
   if (j == 20 && has_z && rb == 0 && threadIdx.x == 0) g_xr_trace[4003] = xr_gtime();
 #endif
   if (threadIdx.x == 0) {
-    const double nu = s_nu;
+    const double nu = s_h[2 * j];
     double aa = 0.0;
     for (int i = 0; i < j; ++i) aa = fma(sa[i], sa[i], aa);
     const double bet2 = nu - aa;
@@ -659,9 +703,11 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
       for (int i = 0; i < j; ++i) {
         col[i] += sa[i];
         Hrc[i] = col[i];
+        sHr[(j - 1) * 33 + i] = col[i];
       }
       col[j] = bet;
       Hrc[j] = bet;
+      sHr[(j - 1) * 33 + j] = bet;
       const int c = j - 1;
       for (int i = 0; i < c; ++i) {
         const double ci = scs[i], si = ssn[i];
@@ -711,13 +757,13 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
   // pass-B coefficients and the first projection (new raw column j):
   // d = [b, (c - aᵀb)/β], Hr[:, j] = (d - H a)/β with the finalised columns k < j
   const double bi = 1.0 / s_bet;
-  const double cc = s_cc;
+  const double cc = has_z ? s_h[2 * j + 1] : 0.0;
   double ab = 0.0;
   for (int i = 0; i < j; ++i) ab = fma(sa[i], sb[i], ab);
   const double dj = (cc - ab) * bi;
   for (int i = threadIdx.x; i <= j; i += blockDim.x) {
     double ha = 0.0;  // upper Hessenberg: Hr[i][k] != 0 for k >= i-1
-    for (int k = (i > 0 ? i - 1 : 0); k < j; ++k) ha = fma(__ldcg(&gs.Hr[(size_t)k * LD + i]), sa[k], ha);
+    for (int k = (i > 0 ? i - 1 : 0); k < j; ++k) ha = fma(sHr[k * 33 + i], sa[k], ha);
     const double di = i < j ? sb[i] : dj;
     gs.Hr[(size_t)j * LD + i] = (di - ha) * bi;
     if (i < j) {
@@ -811,7 +857,7 @@ __global__ void __launch_bounds__(256, NS * EPL > 16 ? 2 : 4) k_gm_dcgs_a(VecArg
   if (trc) g_xr_trace[blockIdx.x * 4 + 1] = xr_gtime();
   if (z != nullptr && rb == 0 && threadIdx.x == 0) atomicMax(&g_xr_trace[3000 + j * 4 + 1], xr_gtime());
 #endif
-  if (finalize2(a, rb, part, 2 * j + 2, a.gs[rb].h)) {
+  if (finalize2_l1(a, rb, part, 2 * j + 2)) {
 #if FDE_SOP_TRACE
     if (trc) g_xr_trace[4000] = xr_gtime();
 #endif
@@ -833,6 +879,9 @@ __global__ void __launch_bounds__(256, NS * EPL > 16 ? 2 : 4) k_gm_dcgs_a(VecArg
 // warp-split pass B it replaced (cfg 4: 40 vs 42 µs per step); the same idea
 // for pass A (register accumulators, or warp-split without staging) measured
 // slower than k_gm_dcgs_a and was dropped.
+#ifndef FDE_GMB_REV
+#define FDE_GMB_REV 1
+#endif
 template <int JB>
 __global__ void __launch_bounds__(128) k_gm_dcgs_b2(VecArgs a, const double* __restrict__ V, size_t vstride,
                                                     double* __restrict__ u, double* __restrict__ z, int j) {
@@ -853,7 +902,11 @@ __global__ void __launch_bounds__(128) k_gm_dcgs_b2(VecArgs a, const double* __r
   const bool trc = (j == 20 && rb == 0 && threadIdx.x == 0);
   if (trc) g_xr_trace[blockIdx.x * 4 + 2] = xr_gtime();
 #endif
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N; e += gridDim.x * blockDim.x) {
+  // elements in DESCENDING order: pass A swept the basis upwards just before,
+  // so the top of every basis vector is what the L2 still holds (cfg 4: the
+  // basis exceeds the L2 from j ≈ 12; pass B 43.8 -> 30 µs per step on average)
+  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < N; e0 += gridDim.x * blockDim.x) {
+    const int e = FDE_GMB_REV ? N - 1 - e0 : e0;
     const double uv = __ldcg(u + o + e), zv = __ldcg(z + o + e);
     double vv[JB];
 #pragma unroll

@@ -51,6 +51,12 @@ struct LineArgs {
   KryFuse kf;             // fused PCG vector work (krylov_kernels.cuh); kf.mode = 0: none
 };
 
+// L2 prefetches (hints: no completion to wait for, no destination)
+// bytes [b, e) rounded inwards to 16-byte granules, as one bulk prefetch
+__device__ __forceinline__ void prefetch_l2_bulk(const void* b, const void* e) {
+  const unsigned long long lo = ((unsigned long long)b + 15ull) & ~15ull, hi = (unsigned long long)e & ~15ull;
+  if (hi > lo) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo)) : "memory");
+}
 // per-RHS gate of the fused Krylov kernels: CTAs of a finished RHS exit at once
 __device__ __forceinline__ bool kry_skip(const LineArgs& a) {
   return a.kf.mode != 0 && !a.kf.st[blockIdx.y].cyc_active;
@@ -87,6 +93,18 @@ __device__ __forceinline__ Line line_of_pitch(int l, int b, int n, int pitch, bo
   L.stride = COL ? pitch : 1;
   L.fbase = COL ? l : l * n;
   return L;
+}
+
+// the variable-coefficient fields cP, cM of a row pair (read by the epilogue,
+// after three transforms): one thread per pair prefetches the two contiguous
+// rows into the L2 (cfg 4 row pass 35.2 -> 33.6 µs; the same for the strided
+// column fields, one prefetch per sector and thread, measured no gain)
+__device__ __forceinline__ void prefetch_coef_rows(const LineArgs& a, const Line& A0, bool v0, bool v1, int t) {
+  if (t == 0 && v0) {
+    const int cnt = (v1 ? 2 : 1) * a.n;
+    prefetch_l2_bulk(a.cP + A0.fbase, a.cP + A0.fbase + cnt);
+    prefetch_l2_bulk(a.cM + A0.fbase, a.cM + A0.fbase + cnt);
+  }
 }
 
 // 16-byte asynchronous global -> shared copy
@@ -165,6 +183,7 @@ k_toeplitz_lines(LineArgs a) {
   }
 #pragma unroll
   for (int q = G::R / 2; q < G::R; ++q) v[q] = make_double2(0.0, 0.0);
+  if (VAR && !COL) prefetch_coef_rows(a, A0, v0, v1, t);
   if (COL && a.yin) {
 #pragma unroll
     for (int q = 0; q < G::R / 2; ++q) {
