@@ -1701,6 +1701,9 @@ fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int ma
 }
 
 // ---------------------------------------------------------------- GMRES
+#ifndef FDE_GMA_NS3
+#define FDE_GMA_NS3 1
+#endif
 #ifndef FDE_GMA_EPL4
 #define FDE_GMA_EPL4 4   // elements per lane of DCGS2 pass A for j >= 16 (4 basis vectors per warp)
 #endif
@@ -1719,7 +1722,12 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
     const dim3 sgrid(std::min(RED_BLOCKS, std::max(1, (va.N + 127) / 128)), h->batch);
     auto pick = [&](int j, auto&& f) {
       if (j < 8) f(std::integral_constant<int, 1>{}, std::integral_constant<int, 16>{}, std::integral_constant<int, 8>{});
-      else if (j < 16) f(std::integral_constant<int, 2>{}, std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{});
+      else if (j <= 16) f(std::integral_constant<int, 2>{}, std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{});
+#if FDE_GMA_NS3
+      // three slots per warp for 17..24 vectors: the four-slot instantiation moves a
+      // quarter of empty slots there (trace: 1.62 µs per vector at j = 15, 1.97 at j = 18)
+      else if (j <= 24) f(std::integral_constant<int, 3>{}, std::integral_constant<int, 5>{}, std::integral_constant<int, 32>{});
+#endif
       else f(std::integral_constant<int, 4>{}, std::integral_constant<int, FDE_GMA_EPL4>{}, std::integral_constant<int, 32>{});
     };
     for (int j = 0; j <= restart; ++j) {

@@ -689,10 +689,11 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
 #if FDE_SOP_TRACE
   if (j == 20 && has_z && rb == 0 && threadIdx.x == 0) g_xr_trace[4003] = xr_gtime();
 #endif
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {   // warp 0: lane-parallel where the step allows, lane 0 for the Givens chain
+    const int ln = threadIdx.x;
     const double nu = s_h[2 * j];
-    double aa = 0.0;
-    for (int i = 0; i < j; ++i) aa = fma(sa[i], sa[i], aa);
+    const double av = ln < j ? sa[ln] : 0.0;
+    const double aa = warp_sum(av * av);   // butterfly order: the same on every lane and every run
     const double bet2 = nu - aa;
     const double bet = bet2 > 0.0 ? sqrt(bet2) : 0.0;
     bool stop = false;
@@ -700,54 +701,62 @@ __device__ __forceinline__ void dcgs_step(VecArgs& a, int rb, int j, bool has_z)
       double* Hrc = gs.Hr + (size_t)(j - 1) * LD;
       double* Hc = gs.H + (size_t)(j - 1) * LD;
       double* col = scol;
-      for (int i = 0; i < j; ++i) {
-        col[i] += sa[i];
-        Hrc[i] = col[i];
-        sHr[(j - 1) * 33 + i] = col[i];
+      if (ln <= j) {   // the raw column: + a (reorthogonalisation), β_j below the diagonal
+        const double cv = ln < j ? col[ln] + av : bet;
+        col[ln] = cv;
+        Hrc[ln] = cv;
+        sHr[(j - 1) * 33 + ln] = cv;
       }
-      col[j] = bet;
-      Hrc[j] = bet;
-      sHr[(j - 1) * 33 + j] = bet;
+      __syncwarp();
       const int c = j - 1;
-      for (int i = 0; i < c; ++i) {
-        const double ci = scs[i], si = ssn[i];
-        const double t = ci * col[i] + si * col[i + 1];
-        col[i + 1] = -si * col[i] + ci * col[i + 1];
-        col[i] = t;
+      double cn = 0.0, sn = 0.0, den = 0.0;
+      if (ln == 0) {   // the rotations of the earlier columns: the running entry stays in a register
+        double x = col[0];
+        for (int i = 0; i < c; ++i) {
+          const double ci = scs[i], si = ssn[i], y = col[i + 1];
+          col[i] = ci * x + si * y;
+          x = -si * x + ci * y;
+        }
+        den = hypot(x, bet);
+        cn = x / den;
+        sn = bet / den;
+        col[c] = den;
+        col[c + 1] = 0.0;
+        gs.cs[c] = cn;
+        gs.sn[c] = sn;
       }
-      const double den = hypot(col[c], col[c + 1]);
-      const double cn = col[c] / den, sn = col[c + 1] / den;
-      gs.cs[c] = cn;
-      gs.sn[c] = sn;
-      col[c] = den;
-      col[c + 1] = 0.0;
-      for (int i = 0; i <= j; ++i) Hc[i] = col[i];
-      const double gc = s_g;
-      gs.g[c + 1] = -sn * gc;
-      gs.g[c] = cn * gc;
-      const int its = s_iters + 1;
-      s.iters = its;
-      s.kused = j;
-      s.rnorm = fabs(sn * gc) / s_bnorm;
-      if (!isfinite(bet) || !isfinite(den)) {
-        s.status = ST_NONFINITE;
-        stop = true;
-      } else if (fabs(sn * gc) <= a.rtol * s_bnorm) {
-        s.converged = 1;
-        stop = true;
-      } else if (bet == 0.0) {
-        s.status = ST_BREAKDOWN;
-        stop = true;
-      } else if (its >= a.maxit || !has_z) {
-        stop = true;  // budget, or the end-of-cycle pass
+      __syncwarp();
+      if (ln <= j) Hc[ln] = col[ln];
+      if (ln == 0) {
+        const double gc = s_g;
+        gs.g[c + 1] = -sn * gc;
+        gs.g[c] = cn * gc;
+        const int its = s_iters + 1;
+        s.iters = its;
+        s.kused = j;
+        s.rnorm = fabs(sn * gc) / s_bnorm;
+        if (!isfinite(bet) || !isfinite(den)) {
+          s.status = ST_NONFINITE;
+          stop = true;
+        } else if (fabs(sn * gc) <= a.rtol * s_bnorm) {
+          s.converged = 1;
+          stop = true;
+        } else if (bet == 0.0) {
+          s.status = ST_BREAKDOWN;
+          stop = true;
+        } else if (its >= a.maxit || !has_z) {
+          stop = true;  // budget, or the end-of-cycle pass
+        }
       }
-    } else if (!(bet > 0.0)) {
+    } else if (ln == 0 && !(bet > 0.0)) {
       s.status = isfinite(bet) ? ST_BREAKDOWN : ST_NONFINITE;
       stop = true;
     }
-    if (stop && s_act) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
-    s_bet = bet;
-    s_stop = stop;
+    if (ln == 0) {
+      if (stop && s_act) { s.cyc_active = 0; atomicSub(&a.ctr->active, 1); }
+      s_bet = bet;
+      s_stop = stop;
+    }
   }
   __syncthreads();
 #if FDE_SOP_TRACE

@@ -99,6 +99,28 @@ def test_gmres_cgs_kernel_variants(torch_cuda, monkeypatch, orth):
             assert relerr(x[b], xo) <= 1e-9, (orth, relerr(x[b], xo))
 
 
+@pytest.mark.parametrize("restart", [1, 2, 8, 16, 17, 24, 25, 31])
+def test_gmres_restart_lengths_match_oracle(torch_cuda, restart):
+    """GMRES(m) at the boundaries of the DCGS2 instantiations (pass A runs 1, 2,
+    3 or 4 basis slots per warp for j <= 8, 16, 24, 31; pass B 8 or 32 slots;
+    DCGS2 itself up to restart 31): iterations within 1 of the oracle's GMRES(m)
+    (P:L519), solution to 1e-9, on a 2D variable-coefficient system (cfg 4
+    shape, n = 127; two RHS at restart 17)."""
+    p = W.config(4, n=127, batch=2 if restart == 17 else 1)
+    s = oracle_system(p)
+    maxit = 400 if restart >= 8 else 60
+    st, stats, x, _ = gpu_solve(torch_cuda, p, "gmres", restart=restart, maxit=maxit)
+    ref = oracle_solve(p, s, "gmres", restart=restart, maxit=maxit)
+    for b in range(p.batch):
+        xo, it_o, conv_o, _ = ref[b]
+        assert bool(stats[b]["converged"]) == bool(conv_o), (restart, b, stats[b], it_o)
+        assert abs(stats[b]["iters"] - it_o) <= 1, (restart, b, stats[b]["iters"], it_o)
+        if conv_o:
+            assert relerr(x[b], xo) <= 1e-9
+        else:   # budget exhausted on both sides: the same iterate up to rounding growth
+            assert relerr(x[b], xo) <= 1e-6
+
+
 def test_gmres_left_unrestarted_matches_oracle(torch_cuda):
     p = W.config(2, n=255, prec=W.PREC_TAU_D)
     s = oracle_system(p)
