@@ -1701,6 +1701,9 @@ fde_status run_pcg(fde_handle h, const double* b, double* x, double rtol, int ma
 }
 
 // ---------------------------------------------------------------- GMRES
+#ifndef FDE_GMB_BPS
+#define FDE_GMB_BPS 6   // pass B blocks per SM (= the kernel's launch bound FDE_GMB_MINB)
+#endif
 #ifndef FDE_GMA_NS3
 #define FDE_GMA_NS3 1
 #endif
@@ -1719,7 +1722,13 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
   if (h->gm_dcgs && restart <= 31) {  // DCGS2: two passes over the basis per step (krylov_kernels.cuh)
     // pass A: warp-split (k_gm_dcgs_a, measured best: the barrier-free a2/a3
     // variants were slower); pass B: streaming, one thread per element (b2)
-    const dim3 sgrid(std::min(RED_BLOCKS, std::max(1, (va.N + 127) / 128)), h->batch);
+    // pass B has no partials: its grid is sized by residency alone (80 registers x 128
+    // threads: FDE_GMB_BPS = 6 blocks per SM for the 32-slot body, twice that for the
+    // 8-slot one). Measured at cfg 4, µs per step of pass B: 4 per SM 35.4, 5 (96
+    // registers) 41.1, 6 31.6, 7 31.3, 8 (64 registers, spills) 39.6; a grid above the
+    // resident count (6 per SM at 96 registers) 37.3
+    auto bgrid = [&](int bps) { return dim3(std::min(RED_BLOCKS / 4 * bps, std::max(1, (va.N + 127) / 128)), h->batch); };
+    const dim3 sgrid = bgrid(FDE_GMB_BPS), sgrid8 = bgrid(2 * FDE_GMB_BPS);
     auto pick = [&](int j, auto&& f) {
       if (j < 8) f(std::integral_constant<int, 1>{}, std::integral_constant<int, 16>{}, std::integral_constant<int, 8>{});
       else if (j <= 16) f(std::integral_constant<int, 2>{}, std::integral_constant<int, 8>{}, std::integral_constant<int, 16>{});
@@ -1760,7 +1769,7 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
         // 35.3 with 32 slots), while at small j the 32-slot one is latency-
         // bound (j = 0: 20.6 vs 11.6 µs)
         (void)jb;
-        if (j < 6) launch_named(h, "gm_dcgs_b", [&] { launch_k(h->st, k_gm_dcgs_b2<8>, sgrid, 128, 0, va, V, vs, Vj, Vn, j); });
+        if (j < 6) launch_named(h, "gm_dcgs_b", [&] { launch_k(h->st, k_gm_dcgs_b2<8>, sgrid8, 128, 0, va, V, vs, Vj, Vn, j); });
         else launch_named(h, "gm_dcgs_b", [&] { launch_k(h->st, k_gm_dcgs_b2<32>, sgrid, 128, 0, va, V, vs, Vj, Vn, j); });
       });
     }

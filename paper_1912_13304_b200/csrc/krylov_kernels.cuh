@@ -888,11 +888,14 @@ __global__ void __launch_bounds__(256, NS * EPL > 16 ? 2 : 4) k_gm_dcgs_a(VecArg
 // warp-split pass B it replaced (cfg 4: 40 vs 42 µs per step); the same idea
 // for pass A (register accumulators, or warp-split without staging) measured
 // slower than k_gm_dcgs_a and was dropped.
+#ifndef FDE_GMB_MINB
+#define FDE_GMB_MINB 6   // 80 registers: six 128-thread blocks per SM, the grid pass B is launched with
+#endif
 #ifndef FDE_GMB_REV
 #define FDE_GMB_REV 1
 #endif
 template <int JB>
-__global__ void __launch_bounds__(128) k_gm_dcgs_b2(VecArgs a, const double* __restrict__ V, size_t vstride,
+__global__ void __launch_bounds__(128, FDE_GMB_MINB) k_gm_dcgs_b2(VecArgs a, const double* __restrict__ V, size_t vstride,
                                                     double* __restrict__ u, double* __restrict__ z, int j) {
   FDE_PDL_ENTRY();
   if (a.ctr->active == 0) return;
