@@ -398,18 +398,31 @@ k_dst_toep_rows(LineArgs a, double* __restrict__ zout) {
     }
     dit_chain<GT, +1>(v, smT, t, twt);
   }
+  constexpr int EB = FDE_EPI_BATCH;   // field loads batched as in k_toeplitz_lines
+  double cf[VAR ? EB : 1][4];
 #pragma unroll
   for (int q = 0; q < GT::R / 2; ++q) {
+    if (VAR && q % EB == 0) {
+#pragma unroll
+      for (int b = 0; b < EB; ++b) {
+        const int pb = ((q + b) << (K - KR_FUSED)) | t;
+        const bool in = q + b < GT::R / 2 && pb < a.n;
+        cf[VAR ? b : 0][0] = (in && v0) ? __ldg(a.cP + A0.fbase + pb) : 0.0;
+        cf[VAR ? b : 0][1] = (in && v0) ? __ldg(a.cM + A0.fbase + pb) : 0.0;
+        cf[VAR ? b : 0][2] = (in && v1) ? __ldg(a.cP + A1.fbase + pb) : 0.0;
+        cf[VAR ? b : 0][3] = (in && v1) ? __ldg(a.cM + A1.fbase + pb) : 0.0;
+      }
+    }
     const int p = (q << (K - KR_FUSED)) | t;
     if (p >= a.n) continue;
-    const int f0 = A0.fbase + p, f1 = A1.fbase + p;
     double r0, r1;
     if (!VAR) {
       r0 = v[q].x;
       r1 = v[q].y;
     } else {
-      r0 = v0 ? __ldg(a.cP + f0) * u[q].x + __ldg(a.cM + f0) * v[q].x : 0.0;
-      r1 = v1 ? __ldg(a.cP + f1) * u[q].y + __ldg(a.cM + f1) * v[q].y : 0.0;
+      const double* c = cf[VAR ? q % EB : 0];
+      r0 = v0 ? c[0] * u[q].x + c[1] * v[q].x : 0.0;
+      r1 = v1 ? c[2] * u[q].y + c[3] * v[q].y : 0.0;
     }
     if (a.nu != 0.0) {
       const double2 zz = sm[GM::swz(p)];

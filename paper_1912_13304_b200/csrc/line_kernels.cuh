@@ -107,6 +107,10 @@ __device__ __forceinline__ void prefetch_coef_rows(const LineArgs& a, const Line
   }
 }
 
+#ifndef FDE_EPI_BATCH
+#define FDE_EPI_BATCH 2   // epilogue positions whose coefficient fields are loaded together (variable Toeplitz passes)
+#endif
+
 // 16-byte asynchronous global -> shared copy
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -237,8 +241,26 @@ k_toeplitz_lines(LineArgs a) {
   double acc[3] = {0.0, 0.0, 0.0};
   const bool pq = (a.kf.mode & KM_PQ) != 0;
 
+  // variable coefficients: the fields of FDE_EPI_BATCH epilogue positions are
+  // loaded together before their products (4 loads per position; the ncu
+  // source page had 37% of the stall samples on these DMULs). cfg 4, µs per
+  // Arnoldi step: batch 2 154.9, 4 155.8, 8 159.3 (spills), unbatched 157.4
+  constexpr int EB = FDE_EPI_BATCH;
+  double cf[VAR ? EB : 1][4];
 #pragma unroll
   for (int q = 0; q < G::R / 2; ++q) {
+    if (VAR && q % EB == 0) {
+#pragma unroll
+      for (int b = 0; b < EB; ++b) {
+        const int pb = ((q + b) << (K - k)) | t;
+        const bool in = q + b < G::R / 2 && pb < n;
+        const int g0 = A0.fbase + pb * A0.stride, g1 = A1.fbase + pb * A1.stride;
+        cf[VAR ? b : 0][0] = (in && v0) ? __ldg(a.cP + g0) : 0.0;
+        cf[VAR ? b : 0][1] = (in && v0) ? __ldg(a.cM + g0) : 0.0;
+        cf[VAR ? b : 0][2] = (in && v1) ? __ldg(a.cP + g1) : 0.0;
+        cf[VAR ? b : 0][3] = (in && v1) ? __ldg(a.cM + g1) : 0.0;
+      }
+    }
     const int p = (q << (K - k)) | t;
     if (p >= n) continue;
     const long long o0 = A0.base + (long long)p * A0.stride, o1 = A1.base + (long long)p * A1.stride;
@@ -252,8 +274,9 @@ k_toeplitz_lines(LineArgs a) {
         if (v1) r1 *= __ldg(a.omul + f1);
       }
     } else {
-      if (v0) r0 = __ldg(a.cP + f0) * u[q].x + __ldg(a.cM + f0) * v[q].x;
-      if (v1) r1 = __ldg(a.cP + f1) * u[q].y + __ldg(a.cM + f1) * v[q].y;
+      const double* c = cf[VAR ? q % EB : 0];
+      if (v0) r0 = c[0] * u[q].x + c[1] * v[q].x;
+      if (v1) r1 = c[2] * u[q].y + c[3] * v[q].y;
     }
     // ν x: folded into μ (ν + λ) for constant coefficients (the host passes
     // nu = 0 then), explicit otherwise; the partial of the other direction is read here with
