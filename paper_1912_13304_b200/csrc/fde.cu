@@ -1803,7 +1803,10 @@ void gmres_cycle(fde_handle h, const VecArgs& va, int restart, int left) {
     }
   }
   // end of cycle: x += P⁻¹(V y) (right) or V y (left); restart residual
-  launch_named(h, "gm_lincomb", [&] { launch_k(h->st, k_gm_lincomb, VGRID, RED_THREADS, 0, va, V, vs, h->kp); });
+  {   // streaming kernel, sized by residency like DCGS2 pass B (six 128-thread blocks per SM)
+    const dim3 lgrid(std::min(RED_BLOCKS / 4 * 6, std::max(1, (va.N + 127) / 128)), h->batch);
+    launch_named(h, "gm_lincomb", [&] { launch_k(h->st, k_gm_lincomb, lgrid, 128, 0, va, V, vs, h->kp); });
+  }
   if (!left) {
     op_tau(h, h->kp, h->kz, gU);
     launch_k(h->st, k_gm_xupd, VGRID, RED_THREADS, 0, va, h->kz, h->kx);

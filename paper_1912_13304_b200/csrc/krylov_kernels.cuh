@@ -940,29 +940,51 @@ __global__ void __launch_bounds__(128, FDE_GMB_MINB) k_gm_dcgs_b2(VecArgs a, con
 }
 
 // end of cycle, step 1: y = R⁻¹ g (redundantly per block), u = Σ y_i V_i
-__global__ void k_gm_lincomb(VecArgs a, const double* __restrict__ V, size_t vstride, double* u) {
+__global__ void __launch_bounds__(128, 6) k_gm_lincomb(VecArgs a, const double* __restrict__ V, size_t vstride, double* u) {
   FDE_PDL_ENTRY();
   if (a.ctr->unfinished == 0) return;
   const int rb = blockIdx.y, N = a.N;
   if (a.st[rb].finished) return;
   const size_t o = (size_t)rb * N;
   __shared__ double ys[MAX_RESTART], ys2[MAX_RESTART];
+  __shared__ double sR[32 * 33], sg[32];   // R and g of a cycle of at most 32 steps
   const int ku = a.st[rb].kused;
+  const GmresSmall& gs = a.gs[rb];
+  constexpr int LD = MAX_RESTART + 1;
+  const bool staged = ku <= 32;
+  if (staged) {   // one round trip for the triangular system (read from global memory
+                  // inside the solve it was ≈ ku dependent round trips in every block)
+    for (int q = threadIdx.x; q < ku * 32; q += blockDim.x) {
+      const int c = q >> 5, i = q & 31;
+      if (i <= c) sR[c * 33 + i] = __ldcg(&gs.H[i + (size_t)c * LD]);
+    }
+    if ((int)threadIdx.x < ku) sg[threadIdx.x] = __ldcg(&gs.g[threadIdx.x]);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const GmresSmall& gs = a.gs[rb];
-    constexpr int LD = MAX_RESTART + 1;
     for (int i = ku - 1; i >= 0; --i) {
-      double acc = gs.g[i];
-      for (int c = i + 1; c < ku; ++c) acc -= gs.H[i + (size_t)c * LD] * ys[c];
-      ys[i] = acc / gs.H[i + (size_t)i * LD];
+      double acc = staged ? sg[i] : gs.g[i];
+      for (int c = i + 1; c < ku; ++c) acc -= (staged ? sR[c * 33 + i] : gs.H[i + (size_t)c * LD]) * ys[c];
+      ys[i] = acc / (staged ? sR[i * 33 + i] : gs.H[i + (size_t)i * LD]);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < ku; i += blockDim.x) ys2[i] = ys[i] * a.gs[rb].vsc[i];  // stored V_i
+  for (int i = threadIdx.x; i < MAX_RESTART; i += blockDim.x) ys2[i] = i < ku ? ys[i] * gs.vsc[i] : 0.0;  // stored V_i
   __syncthreads();
-  FDE_GRID_LOOP(e) {
+  // streaming, as pass B: one element per thread and trip, up to 32 basis values
+  // in flight, elements in descending order (the end-of-cycle pass A, which runs
+  // just before, leaves the top of the basis in the L2); the sum runs over i
+  // ascending as before
+  for (long long e0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; e0 < N; e0 += (long long)gridDim.x * blockDim.x) {
+    const long long e = N - 1 - e0;
     double acc = 0.0;
-    for (int i = 0; i < ku; ++i) acc = fma(ys2[i], __ldg(V + (size_t)i * vstride + o + e), acc);
+    for (int i0 = 0; i0 < ku; i0 += 32) {
+      double vv[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) vv[i] = i0 + i < ku ? __ldcg(V + (size_t)(i0 + i) * vstride + o + e) : 0.0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc = fma(ys2[i0 + i], vv[i], acc);
+    }
     u[o + e] = acc;
   }
 }
