@@ -187,6 +187,11 @@ bool is_device_ptr(const void* p) {
 }
 
 // ------------------------------------------------------- launch geometry
+#ifndef FDE_TOEP_COL_FPC
+// column Toeplitz pass: adjacent line pairs per CTA. Measured at cfg 4 (µs per pass): 1 pair (half a
+// 32-byte sector per row) 59.7, 2 pairs 36.2, 4 pairs (512 threads, one CTA per SM) 40.5
+#define FDE_TOEP_COL_FPC 2
+#endif
 template <int K, bool COL, int NBUF>
 struct LaunchCfg {
   using G = FftGeom<K, KR>;
@@ -197,7 +202,7 @@ struct LaunchCfg {
   // rows: ~128 threads per CTA (one line pair at n = 1023), so that every pair of
   // a pass is resident at once; columns: >= 2 adjacent pairs (4 columns = one
   // 32-byte sector per row) per CTA
-  static constexpr int WANT = COL ? (128 / G::P > 2 ? 128 / G::P : 2) : (128 / G::P > 1 ? 128 / G::P : 1);
+  static constexpr int WANT = COL ? (128 / G::P > FDE_TOEP_COL_FPC ? 128 / G::P : FDE_TOEP_COL_FPC) : (128 / G::P > 1 ? 128 / G::P : 1);
   static constexpr int FPC = WANT < BY_SMEM ? (WANT < BY_THR ? WANT : BY_THR) : (BY_SMEM < BY_THR ? BY_SMEM : BY_THR);
   static constexpr int THREADS = FPC * G::P;
   static constexpr int SMEM = FPC * SPG + TW_SMEM_QUARTER * (G::L / 4) * 16;   // + the quarter twiddle table
