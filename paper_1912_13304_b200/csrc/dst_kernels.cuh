@@ -349,6 +349,10 @@ k_dst_toep_rows(LineArgs a, double* __restrict__ zout) {
   __syncthreads();
   double2 v[GT::R];
   const double osc = a.oscale != 0.0 ? a.oscale : 1.0;
+  // output rows of z and of the row partial y: the user layout (pitch n), or pitch
+  // opitch (the column pass then reads aligned column pairs, LineArgs::cpitch)
+  const long long ob0 = a.opitch ? ((long long)blockIdx.y * a.n + (v0 ? l0 : 0)) * a.opitch : A0.base;
+  const long long ob1 = a.opitch ? ((long long)blockIdx.y * a.n + (v1 ? l1 : 0)) * a.opitch : A1.base;
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int e = t + P * i;
@@ -363,8 +367,8 @@ k_dst_toep_rows(LineArgs a, double* __restrict__ zout) {
       }
       if (!v0) z0 = 0.0;
       if (!v1) z1 = 0.0;
-      if (v0) zout[A0.base + e] = z0;
-      if (v1) zout[A1.base + e] = z1;
+      if (v0) zout[ob0 + e] = z0;
+      if (v1) zout[ob1 + e] = z1;
       sm[GM::swz(e)] = make_double2(z0, z1);
     }
     v[i] = make_double2(z0, z1);
@@ -429,8 +433,8 @@ k_dst_toep_rows(LineArgs a, double* __restrict__ zout) {
       r0 = fma(a.nu, zz.x, r0);
       r1 = fma(a.nu, zz.y, r1);
     }
-    if (v0) a.y[A0.base + p] = r0;
-    if (v1) a.y[A1.base + p] = r1;
+    if (v0) a.y[ob0 + p] = r0;
+    if (v1) a.y[ob1 + p] = r1;
   }
 }
 

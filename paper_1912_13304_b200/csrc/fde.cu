@@ -187,6 +187,9 @@ bool is_device_ptr(const void* p) {
 }
 
 // ------------------------------------------------------- launch geometry
+#ifndef FDE_GM_INTERNAL
+#define FDE_GM_INTERNAL 1   // GMRES operator: z and the row partial at pitch m between the Toeplitz passes
+#endif
 #ifndef FDE_TOEP_COL_FPC
 // column Toeplitz pass: adjacent line pairs per CTA. Measured at cfg 4 (µs per pass): 1 pair (half a
 // 32-byte sector per row) 59.7, 2 pairs 36.2, 4 pairs (512 threads, one CTA per SM) 40.5
@@ -311,6 +314,7 @@ struct fde_handle_s {
   const double *sop_maps_z = nullptr, *sop_maps_p = nullptr;
   double *lamS_x = nullptr, *lamK_x = nullptr, *lamS_y = nullptr, *lamK_y = nullptr;
   double *cP_x = nullptr, *cM_x = nullptr, *cP_y = nullptr, *cM_y = nullptr;
+  double *cP_ym = nullptr, *cM_ym = nullptr;   // the column fields at row pitch m (GMRES operator's internal layout)
   double *invF = nullptr, *Fx = nullptr, *Fy = nullptr;
   double fscale = 0.0;
   double *dpre = nullptr, *dpost = nullptr;
@@ -516,9 +520,11 @@ void init_kernel_attrs() {
 }
 
 // One Toeplitz pass along rows (COL=false) or columns (COL=true).
+// cpitch > 0 (column pass of the GMRES operator): x and yin have row pitch cpitch (op_tau_matvec)
 void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const double* yin, double nu, const int* gate,
-                   const KryFuse* kf = nullptr) {
+                   const KryFuse* kf = nullptr, int cpitch = 0) {
   LineArgs a = base_args(h);
+  a.cpitch = col ? cpitch : 0;
   if (kf) a.kf = *kf;
   a.x = x;
   a.y = y;
@@ -536,8 +542,8 @@ void toeplitz_pass(fde_handle h, bool col, const double* x, double* y, const dou
   }
   a.lamS = col ? h->lamS_y : h->lamS_x;
   a.lamK = col ? h->lamK_y : h->lamK_x;
-  a.cP = col ? h->cP_y : h->cP_x;
-  a.cM = col ? h->cM_y : h->cM_x;
+  a.cP = col ? (a.cpitch ? h->cP_ym : h->cP_y) : h->cP_x;
+  a.cM = col ? (a.cpitch ? h->cM_ym : h->cM_y) : h->cM_x;
   bool fused = false;
   FDE_SWITCH_K(h->K, (fused = var_fused_fits<KK>()));
   if (fused) {
@@ -881,9 +887,19 @@ void op_tau_matvec(fde_handle h, const double* v, double* z, double* y, const in
   }
   c.x = h->t2;
   c.pitch = xpitch;
+  // internal layout between the two Toeplitz passes: z (into t1, free after the τ core) and
+  // the row partial (wx) at row pitch m, so the column pass reads 16-byte aligned column
+  // pairs of z, the partial and the fields (half the load instructions of a pass that is
+  // bound by them); the caller's z is then NOT written (GMRES does not read it)
+  bool internal = h->stau_ok && FDE_GM_INTERNAL;
+  if (internal && h->var_y) { FDE_SWITCH_K(h->K, (internal = var_fused_fits<KK>())); }
+  if (internal) {
+    c.opitch = h->m;
+    z = h->t1;
+  }
   if (var) { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, false, true>(h, c, z))); }
   else { FDE_SWITCH_K(h->K, (launch_dst_toep_k<KK, false, false>(h, c, z))); }
-  toeplitz_pass(h, true, z, y, h->wx, 0.0, gate);
+  toeplitz_pass(h, true, z, y, h->wx, 0.0, gate, nullptr, internal ? h->m : 0);
 }
 
 // ------------------------------------------------------------- create
@@ -1199,6 +1215,15 @@ void build(fde_handle h, const fde_desc* d) {
   h->t2 = h->dalloc<double>(ve);
   h->t3 = h->dalloc<double>(ve);
   if (h->stau_ok) FDE_CUDA(fde::sop::make_stau_maps(&h->stau_maps, h->t1, h->t2, n, h->batch));
+  if (h->stau_ok && h->var_y) {   // column fields at row pitch m (padding column zero)
+    const size_t fe = (size_t)n * m;
+    h->cP_ym = h->dalloc<double>(fe);
+    h->cM_ym = h->dalloc<double>(fe);
+    FDE_CUDA(cudaMemsetAsync(h->cP_ym, 0, fe * sizeof(double), h->st));
+    FDE_CUDA(cudaMemsetAsync(h->cM_ym, 0, fe * sizeof(double), h->st));
+    launch_k(h->st, k_repitch, dim3(std::min(n, 1024), 1), 256, 0, (const double*)h->cP_y, h->cP_ym, n, n, m);
+    launch_k(h->st, k_repitch, dim3(std::min(n, 1024), 1), 256, 0, (const double*)h->cM_y, h->cM_ym, n, n, m);
+  }
   h->hin = h->dalloc<double>(ve);
   h->hout = h->dalloc<double>(ve);
   h->sst = h->dalloc<SolveState>(h->batch);

@@ -49,6 +49,11 @@ struct LineArgs {
   int persist;            // sine-domain 1D body (MODE 5): loop inside the kernel until the RHS finishes
   int pitch;              // sine-domain kernels: row pitch of the internal 2D vectors (0 = n)
   KryFuse kf;             // fused PCG vector work (krylov_kernels.cuh); kf.mode = 0: none
+  // GMRES operator, internal layout: cpitch > 0 (= m, even) — the column
+  // Toeplitz pass reads x, yin and the fields cP, cM at row pitch cpitch (column pairs are
+  // 16-byte aligned: one 16-byte access per pair and row); opitch > 0 — k_dst_toep_rows
+  // writes z and its row partial y at row pitch opitch
+  int cpitch, opitch;
 };
 
 // L2 prefetches (hints: no completion to wait for, no destination)
@@ -170,11 +175,20 @@ k_toeplitz_lines(LineArgs a) {
   double2 v[G::R];
   const bool pupd = (a.kf.mode & KM_PUPD) != 0;
   const double beta = pupd ? a.kf.st[blockIdx.y].betac : 0.0;
+  // internal-layout column pass: element (row p, columns l0, l0+1) of RHS b at cb + p·cpitch
+  const bool cvec = COL && a.cpitch > 0;
+  const long long cb = cvec ? (long long)blockIdx.y * n * a.cpitch + (v0 ? l0 : 0) : 0;
 #pragma unroll
   for (int q = 0; q < G::R / 2; ++q) {
     const int p = (q << (K - k)) | t;
     double re = 0.0, im = 0.0;
-    if (p < n) {
+    if (cvec) {
+      if (p < n) {
+        const double2 w = __ldg(reinterpret_cast<const double2*>(a.x + cb + (long long)p * a.cpitch));
+        re = v0 ? w.x : 0.0;
+        im = v1 ? w.y : 0.0;
+      }
+    } else if (p < n) {
       const long long o0 = A0.base + (long long)p * A0.stride, o1 = A1.base + (long long)p * A1.stride;
       if (v0) re = __ldg(a.x + o0);
       if (v1) im = __ldg(a.x + o1);
@@ -193,8 +207,12 @@ k_toeplitz_lines(LineArgs a) {
     for (int q = 0; q < G::R / 2; ++q) {
       const int p = (q << (K - k)) | t;
       if (p < n) {
-        if (v0) cp_async8(&smY[p].x, a.yin + A0.base + (long long)p * A0.stride);
-        if (v1) cp_async8(&smY[p].y, a.yin + A1.base + (long long)p * A1.stride);
+        if (cvec) {
+          cp_async16(&smY[p], a.yin + cb + (long long)p * a.cpitch);
+        } else {
+          if (v0) cp_async8(&smY[p].x, a.yin + A0.base + (long long)p * A0.stride);
+          if (v1) cp_async8(&smY[p].y, a.yin + A1.base + (long long)p * A1.stride);
+        }
       }
     }
   }
@@ -254,6 +272,16 @@ k_toeplitz_lines(LineArgs a) {
       for (int b = 0; b < EB; ++b) {
         const int pb = ((q + b) << (K - k)) | t;
         const bool in = q + b < G::R / 2 && pb < n;
+        if (cvec) {   // fields at pitch cpitch (shared by all RHS): both columns in one access
+          const long long g = (long long)pb * a.cpitch + (v0 ? l0 : 0);
+          const double2 wp = in ? __ldg(reinterpret_cast<const double2*>(a.cP + g)) : make_double2(0.0, 0.0);
+          const double2 wm = in ? __ldg(reinterpret_cast<const double2*>(a.cM + g)) : make_double2(0.0, 0.0);
+          cf[VAR ? b : 0][0] = wp.x;
+          cf[VAR ? b : 0][1] = wm.x;
+          cf[VAR ? b : 0][2] = wp.y;
+          cf[VAR ? b : 0][3] = wm.y;
+          continue;
+        }
         const int g0 = A0.fbase + pb * A0.stride, g1 = A1.fbase + pb * A1.stride;
         cf[VAR ? b : 0][0] = (in && v0) ? __ldg(a.cP + g0) : 0.0;
         cf[VAR ? b : 0][1] = (in && v0) ? __ldg(a.cM + g0) : 0.0;
