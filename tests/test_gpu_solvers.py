@@ -228,6 +228,23 @@ def test_batch_rhs_are_independent_and_deterministic(torch_cuda, monkeypatch, so
             assert np.array_equal(x1[0], x3[b]), (cfg, b)
 
 
+def test_gmres_batch_independent_in_the_internal_layout(torch_cuda):
+    """2D variable-coefficient GMRES at m = 512 (the τ passes on the r02
+    transform engine, z and the row partial at row pitch m between the two
+    Toeplitz passes): a batch-2 solve equals the two single-RHS solves bitwise
+    (per-RHS grids, per-RHS fixed-order reductions; the single-RHS solve at
+    this size is compared with the oracle in test_solver_parity), iteration
+    budget of three cycles."""
+    p = W.config(4, n=511, batch=2)
+    _, st2, x2, _ = gpu_solve(torch_cuda, p, "gmres", maxit=90)
+    for b in range(2):
+        q = W.config(4, n=511, batch=1)
+        q.rhs = p.rhs[b:b + 1].copy()
+        _, st1, x1, _ = gpu_solve(torch_cuda, q, "gmres", maxit=90)
+        assert st1[0]["iters"] == st2[b]["iters"]
+        assert np.array_equal(x1[0], x2[b]), b
+
+
 def test_not_converged_status_keeps_last_iterate(torch_cuda):
     from paper_1912_13304_b200 import fde
     p = W.config(5, n=255)

@@ -13,10 +13,10 @@ FDE_GRAPH=0 python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/
 FDE_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; echo "ncu1 rc=$?"
 python tools/ncu_summary.py launches gpurun_out/launches.csv > gpurun_out/launches.txt 2>&1
-FDE_GRAPH=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_sop|k_sine_xr5" -s 4 -c 2 \
+FDE_GRAPH=0 timeout 600 ncu --set full --clock-control none --import-source on -f -k regex:"k_sop|k_sine_xr5" -s 4 -c 2 \
     -o /tmp/prof_iter python tools/unit_run.py --reps 1 --pcg > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"
 python tools/ncu_summary.py full /tmp/prof_iter.ncu-rep --traffic gpurun_out/traffic_1023.json > gpurun_out/ncu_full_iter.txt 2>&1
 python tools/ncu_source.py /tmp/prof_iter.ncu-rep k_sop > gpurun_out/ncu_sop_source.txt 2>&1
-FDE_GRAPH=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_toeplitz|k_stau|k_dst_toep" -s 4 -c 4 \
+FDE_GRAPH=0 timeout 600 ncu --set full --clock-control none --import-source on -f -k regex:"k_toeplitz|k_stau|k_dst_toep" -s 4 -c 4 \
     -o /tmp/prof_cfg4op python tools/unit_run.py --cfg 4 --n 1023 --reps 0 --gmres 4 > gpurun_out/ncu_cfg4.log 2>&1; echo "ncu3 rc=$?"
 python tools/ncu_summary.py full /tmp/prof_cfg4op.ncu-rep > gpurun_out/ncu_cfg4_summary.txt 2>&1
