@@ -55,9 +55,12 @@ struct FdeFail {
 // launch (PDL) measured slower on the B200 in r01 (cfg 5 n=1023 11.2k vs
 // 11.5k PCG it/s, cfg 3 69.6 vs 51.5 µs/iteration: the early-launched
 // dependent CTAs hold SM slots while they wait), so it is not requested.
-constexpr bool g_pdl = false;
+#ifndef FDE_PDL
+#define FDE_PDL 0
+#endif
+constexpr bool g_pdl = FDE_PDL != 0;
 template <typename... KArgs, typename... Args>
-void launch_k(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+void launch_k_attr(bool pdl, cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -65,10 +68,23 @@ void launch_k(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, si
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   FDE_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+template <typename... KArgs, typename... Args>
+void launch_k(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  launch_k_attr(g_pdl, st, kern, grid, block, smem, args...);
+}
+// the one launch that asks for PDL (r02): the vector step of the r02 sine body, whose CTAs
+// then park in griddepcontrol.wait while the operator kernel's last units drain
+#ifndef FDE_PDL_XR
+#define FDE_PDL_XR 1
+#endif
+template <typename... KArgs, typename... Args>
+void launch_k_pdl(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  launch_k_attr(FDE_PDL_XR != 0, st, kern, grid, block, smem, args...);
 }
 
 #ifndef FDE_KR
@@ -1595,7 +1611,7 @@ void sine_iteration(fde_handle h, double rtol, int maxit) {
     const double* sp = h->spart;
     const int n = h->n, nsp = h->m;   // one p̂·q̂ partial per unit, m units per RHS
     launch_named(h, "sine_xr_sop", [&] {
-      launch_k(h->st, k_sine_xr5, dim3(XR_GRID, h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc, hx, hy, sp, nsp);
+      launch_k_pdl(h->st, k_sine_xr5, dim3(XR_GRID, h->batch), 256, 0, kv, n, lgp, Fx, Fy, wr, wc, hx, hy, sp, nsp);
     });
     return;
   }
