@@ -1409,9 +1409,12 @@ void ensure_krylov(fde_handle h, int nvecV) {
 // gates), so the `unroll` copies after convergence cost only their empty
 // launches, while the WHILE node's per-body re-evaluation (≈8 µs measured on
 // the B200 between k_loop_ctrl and the next body's first kernel) is paid once
-// per `unroll` iterations.
+// per `unroll` iterations. Re-measured at the end of r02 (µs per iteration, 4 / 6 / 8
+// per body): n = 255 25.85 / 25.5 / 25.4, 511 27.5 / 27.0 / 27.0, 1023 52.8 / 52.2 /
+// 52.1, 2047 190.5 / 189.6 / 189.3, cfg 3 (24 iterations) 28.9 / – / 28.3; batch 8
+// at n = 255 (26 iterations) 56.6 / 56.6 / 57.0.
 #ifndef FDE_PCG_UNROLL
-#define FDE_PCG_UNROLL 4
+#define FDE_PCG_UNROLL 8
 #endif
 template <class F>
 int build_while_graph(fde_handle h, cudaGraphExec_t* out, int maxloops, F&& body, int unroll = 1) {
